@@ -1,0 +1,139 @@
+/*
+ * hapod_b200.h -- C-ABI of libhapod_b200.so, the sm_100a kernels behind the
+ * HAPOD hot path (arXiv:1607.05210).
+ *
+ * The reference package (hapod v0.1.0, pure Python + NumPy/SciPy) has no FFI:
+ * its per-node arithmetic is NumPy `@` (BLAS dgemm) and scipy.linalg.eigh
+ * (LAPACK dsyevr).  Each entry point below replaces one of those call sites;
+ * the Python host package `paper_1607_05210_b200` binds them with ctypes and
+ * keeps the reference's Python entry points (pod, block_gramian_pod,
+ * run_hapod, run_parallel, IncrementalSession ...).
+ *
+ * Conventions
+ *   - all matrices float64, column-major, leading dimension >= rows;
+ *   - all data pointers are DEVICE pointers; `stream` is a cudaStream_t;
+ *   - calls are stream-ordered and asynchronous unless stated otherwise;
+ *   - every call returns an hp_status; hp_last_error() gives the message
+ *     (thread-local).  HP_EINVAL maps to ValueError, HP_ELINALG to
+ *     numpy.linalg.LinAlgError (CLI exit 3, cli.py:572-574), HP_ECUDA to
+ *     RuntimeError;
+ *   - workspaces are caller-allocated; query their size with the matching
+ *     *_workspace_bytes function.
+ */
+#ifndef HAPOD_B200_H
+#define HAPOD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_ABI_VERSION 1
+
+enum hp_status { HP_OK = 0, HP_EINVAL = 1, HP_ECUDA = 2, HP_ELINALG = 3, HP_ENOMEM = 4 };
+
+/* A set of contiguous float64 vectors: vector i starts at table[i] when
+ * table != NULL (a device array of pointers), else at base + i*ld.  Used to
+ * read a node's input as the concatenation of its children's mode blocks
+ * without the hstack copy of hierarchy.py:286-290.  aligned16 != 0 promises
+ * every vector start is 16-byte aligned (enables 16-byte async copies). */
+typedef struct hp_vecset {
+  const double* base;
+  int64_t ld;
+  const double* const* table;
+  int aligned16;
+} hp_vecset;
+
+int hp_abi_version(void);
+const char* hp_last_error(void);
+int hp_device_sm_count(int device);
+
+/* Generic FP64 DMMA GEMM  C = alpha * op(A) op(B) + beta * C, then
+ * C(m,n) *= row_scale[m] * col_scale[n], C(m,n) /= col_div[n] (each nullable).
+ *   a_kmajor: A(m,k) = A.vec(m)[k]  else A(m,k) = A.vec(k)[m]
+ *   b_kmajor: B(k,n) = B.vec(n)[k]  else B(k,n) = B.vec(k)[n]
+ *   sym:      M == N, only the upper triangle is computed and mirrored
+ *   b_upper:  B is upper triangular (B(k,n) = 0 for k > n)
+ * Long contractions are split over K with a fixed-order reduction
+ * (deterministic; the plan depends only on M, N, K). */
+size_t hp_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+int hp_gemm(int a_kmajor, int b_kmajor, int64_t M, int64_t N, int64_t K, hp_vecset A, hp_vecset B, double alpha,
+            double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+            const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, void* stream);
+
+/* K1 -- Gramian G = D S^T S D, D = diag(colscale) (nullable), exactly
+ * symmetric.  Replaces gramian() / InnerProductSpace.gram
+ * (pod.py:208-211, 87-91); with colscale = sigma it is the Gramian of
+ * ModeSet.scaled() (pod.py:160-162) without the copy. */
+size_t hp_gram_workspace_bytes(int64_t d, int64_t m);
+int hp_gram(hp_vecset S, int64_t d, int64_t m, const double* colscale, double* G, int64_t ldg, void* ws,
+            size_t ws_bytes, void* stream);
+
+/* K1b -- block Gramian of [Phi*diag(sigma) | F*diag(fscale)] for the
+ * incremental merge (pod.py:376-384): top-left diag(sigma^2) written down,
+ * mixed block sigma o (Phi^T F), fresh block F^T F, exactly symmetric.
+ * fscale nullable. */
+size_t hp_block_gram_workspace_bytes(int64_t d, int64_t n_old, int64_t m);
+int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F, const double* fscale, int64_t m,
+                  int64_t d, double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream);
+
+/* K2 -- all eigenpairs of the symmetric n x n G, eigenvalues descending,
+ * first nvec eigenvectors in V.  Replaces scipy.linalg.eigh + reversal
+ * (pod.py:329-331, 386-388).  Parallel two-sided block Jacobi; synchronises
+ * the stream once per sweep.  Returns HP_ELINALG if max_sweeps is reached. */
+size_t hp_syev_workspace_bytes(int64_t n);
+int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, void* ws, size_t ws_bytes, void* stream);
+
+/* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
+ * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank
+ * whose tail sum_{n>=N} sigma_n^2 <= eps^2, tail = sum lam_keep[N:].
+ * info4 (device) = {lam_max, nkeep, N, tail}. */
+int hp_truncate(const double* lam_desc, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info4,
+                void* stream);
+
+/* K4 -- mode reconstruction U = (S V[:, :N]) / sigma[:N]  (pod.py:333-334).
+ * For column-scaled inputs pre-scale the rows of V. */
+size_t hp_assemble_workspace_bytes(int64_t d, int64_t m, int64_t N);
+int hp_assemble(hp_vecset S, int64_t d, int64_t m, const double* V, int64_t ldv, const double* sigma, int64_t N,
+                double* U, int64_t ldu, void* ws, size_t ws_bytes, void* stream);
+
+/* K5a -- C = U^T U and drift = max |C - I| (pod.py:245-247), drift_out device scalar. */
+size_t hp_drift_workspace_bytes(int64_t d, int64_t N);
+int hp_drift(const double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double* drift_out, void* ws,
+             size_t ws_bytes, void* stream);
+
+/* K5b -- U <- Q factor of U (CholQR2, shifted CholQR3 on breakdown): the same
+ * span and Gram-Schmidt column order as the MGS sweep of pod.py:227-237.
+ * C = U^T U on entry (destroyed).  Synchronises the stream. */
+size_t hp_reortho_workspace_bytes(int64_t d, int64_t N);
+int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, int* passes_out,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* K6 -- sign convention (pod.py:214-224): per column, the largest-|.| entry
+ * (first index on ties) made positive; R (m_r x N, nullable) flipped alike;
+ * sign_out (nullable) receives the +-1 applied. */
+int hp_signs(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
+             void* stream);
+
+/* Layout helpers: row-major (NumPy C-order) upload -> column-major, row/column
+ * scaling (weighted spaces: InnerProductSpace.weigh/unweigh pod.py:76-84),
+ * finiteness check (SnapshotBlock, pod.py:115-116; bad = device int). */
+int hp_transpose_rm_to_cm(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd, void* stream);
+int hp_scale(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* row_mul, const double* row_div,
+             const double* col_mul, double* dst, int64_t ldd, void* stream);
+int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, void* stream);
+
+/* Deterministic sum of squares of a column-major block (residual energy of
+ * actual_mean_error, hierarchy.py:237-253); out = device scalar. */
+size_t hp_sumsq_workspace_bytes(void);
+int hp_sumsq(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, void* ws, size_t ws_bytes,
+             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HAPOD_B200_H */

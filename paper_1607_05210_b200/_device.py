@@ -1,0 +1,386 @@
+"""Device-side data layout and the per-node POD pipeline on the B200.
+
+Layout in HBM: every snapshot or mode block is a column-major float64 matrix
+whose column stride ``ld`` is ``rows`` rounded up to an even count (16-byte
+aligned columns, so the GEMM engine can use 16-byte async copies).  Storage
+is a torch tensor of shape (cols, ld) -- torch is used for allocation and
+streams only; every arithmetic step is a kernel of libhapod_b200.so.
+
+A node's input is a list of *parts* (DevMat, optional per-column scale).  The
+concatenation is never materialised: the Gram and reconstruction kernels read
+the columns through a device pointer table, and the sigma scaling of
+ModeSet.scaled() (pod.py:160-162) is applied as an epilogue scale (Gram) or
+folded into the eigenvector rows (reconstruction).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+DRIFT_TOL = 1e-8          # pod.py:247
+JACOBI_TOL_REL = 2.0 ** -52
+JACOBI_TOL_ABS = 16 * 2.0 ** -52  # absolute off-diagonal trigger, x max|g_ii| (Gram rounding floor)
+JACOBI_MAX_SWEEPS = 60
+
+
+def require_cuda():
+    if torch is None or not torch.cuda.is_available():
+        raise RuntimeError("the HAPOD B200 path needs a CUDA device (there is no CPU fallback)")
+    N.load()
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def _even(n: int) -> int:
+    return n + (n & 1)
+
+
+class DevMat:
+    """Column-major float64 matrix on the current CUDA device."""
+
+    __slots__ = ("storage", "rows", "cols", "ld", "offset")
+
+    def __init__(self, storage, rows: int, cols: int, ld: int, offset: int = 0):
+        self.storage = storage  # 1-d float64 CUDA tensor
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.ld = int(ld)
+        self.offset = int(offset)  # element offset of column 0
+
+    @staticmethod
+    def empty(rows: int, cols: int, zero: bool = False):
+        ld = max(_even(rows), 2)
+        n = max(ld * cols, 1)
+        st = torch.zeros(n, dtype=torch.float64, device="cuda") if zero else \
+            torch.empty(n, dtype=torch.float64, device="cuda")
+        return DevMat(st, rows, cols, ld)
+
+    @property
+    def ptr(self) -> int:
+        return self.storage.data_ptr() + 8 * self.offset
+
+    def col_ptr(self, j: int) -> int:
+        return self.ptr + 8 * self.ld * j
+
+    def view_cols(self, j0: int, j1: int) -> "DevMat":
+        return DevMat(self.storage, self.rows, j1 - j0, self.ld, self.offset + j0 * self.ld)
+
+    def aligned16(self) -> bool:
+        return self.ld % 2 == 0 and self.ptr % 16 == 0
+
+    def vecset(self) -> N.VecSet:
+        return N.VecSet(self.ptr, self.ld, None, int(self.aligned16()))
+
+    def tensor(self):
+        """(rows, cols) torch view (column-major strides)."""
+        if self.cols == 0:
+            return torch.zeros((self.rows, 0), dtype=torch.float64, device=self.storage.device)
+        return self.storage.as_strided((self.rows, self.cols), (1, self.ld), self.offset)
+
+    def to_numpy(self) -> np.ndarray:
+        if self.cols == 0 or self.rows == 0:
+            return np.zeros((self.rows, self.cols))
+        t = self.storage.as_strided((self.cols, self.rows), (self.ld, 1), self.offset)
+        host = t.cpu().numpy()  # (cols, rows) C-order == (rows, cols) F-order
+        return np.asfortranarray(host.T)
+
+    def clone(self) -> "DevMat":
+        out = DevMat.empty(self.rows, self.cols)
+        if self.cols and self.rows:
+            N.check(N.load().hp_scale(self.ptr, self.ld, self.rows, self.cols, None, None, None,
+                                      out.ptr, out.ld, _stream()), "copy")
+        return out
+
+
+def upload(values, check_finite: bool = True) -> DevMat:
+    """Host (numpy / torch CPU) or device (torch CUDA) d x m array -> DevMat.
+
+    F-contiguous inputs are copied straight into the column-major layout;
+    C-contiguous ones are staged and transposed on the device."""
+    require_cuda()
+    lib = N.load()
+    if torch.is_tensor(values):
+        t = values.detach()
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+    else:
+        a = np.asarray(values, dtype=np.float64)
+        t = torch.from_numpy(a) if (a.flags.c_contiguous or a.flags.f_contiguous) else \
+            torch.from_numpy(np.ascontiguousarray(a))
+    if t.dim() != 2:
+        raise ValueError(f"snapshot block must be 2-d, got shape {tuple(t.shape)}")
+    d, m = int(t.shape[0]), int(t.shape[1])
+    out = DevMat.empty(d, m)
+    if d and m:
+        if t.stride(0) == 1 and t.stride(1) == d:            # column-major source
+            src = t.as_strided((m, d), (d, 1))
+            dst = out.storage[: out.ld * m].view(m, out.ld)[:, :d]
+            dst.copy_(src, non_blocking=True)
+        else:                                                  # row-major (or strided) source
+            tc = t.contiguous() if not (t.is_cuda and t.is_contiguous()) else t
+            dev = tc.to("cuda", non_blocking=True) if not tc.is_cuda else tc
+            N.check(lib.hp_transpose_rm_to_cm(dev.data_ptr(), d, m, out.ptr, out.ld, _stream()),
+                    "upload transpose")
+            if not tc.is_cuda:
+                torch.cuda.current_stream().synchronize()  # keep the staging buffer alive
+        if check_finite:
+            bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+            N.check(lib.hp_finite_check(out.ptr, out.ld, d, m, bad.data_ptr(), _stream()), "finite")
+            if int(bad.item()):
+                raise ValueError("snapshot block contains non-finite entries")
+    return out
+
+
+def ones(n: int):
+    return torch.ones(max(n, 1), dtype=torch.float64, device="cuda")[:n]
+
+
+@dataclass
+class Part:
+    """One column block of a node input: columns mat[:, j] * scale[j]."""
+
+    mat: DevMat
+    scale: object = None  # 1-d float64 CUDA tensor or None (= all ones)
+
+
+def _concat_parts(parts: list[Part]):
+    """VecSet over the concatenated columns + the concatenated scale (or None)."""
+    parts = [p for p in parts if p.mat.cols]
+    m = sum(p.mat.cols for p in parts)
+    if len(parts) == 1 and parts[0].scale is None:
+        return parts[0].mat.vecset(), None, m, parts
+    table = np.empty(m, dtype=np.int64)
+    at = 0
+    aligned = True
+    for p in parts:
+        c = p.mat.cols
+        table[at:at + c] = p.mat.ptr + 8 * p.mat.ld * np.arange(c, dtype=np.int64)
+        aligned &= p.mat.aligned16()
+        at += c
+    tdev = torch.from_numpy(table).to("cuda", non_blocking=True)
+    any_scale = any(p.scale is not None for p in parts)
+    scale = None
+    if any_scale:
+        scale = torch.cat([p.scale if p.scale is not None else ones(p.mat.cols) for p in parts])
+    vs = N.VecSet(0, 0, tdev.data_ptr(), int(aligned))
+    return vs, scale, m, (parts, tdev)
+
+
+def weigh_parts(parts: list[Part], sqrt_w) -> list[Part]:
+    """Euclidean coordinates of weighted snapshots (InnerProductSpace.weigh, pod.py:76-80)."""
+    lib = N.load()
+    out = []
+    for p in parts:
+        x = DevMat.empty(p.mat.rows, p.mat.cols)
+        if p.mat.cols:
+            N.check(lib.hp_scale(p.mat.ptr, p.mat.ld, p.mat.rows, p.mat.cols, sqrt_w.data_ptr(), None,
+                                 None, x.ptr, x.ld, _stream()), "weigh")
+        out.append(Part(x, p.scale))
+    return out
+
+
+def _ws(nbytes: int):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
+
+
+@dataclass
+class NodeOutput:
+    U: DevMat | None
+    sigmas: np.ndarray
+    sigmas_dev: object
+    tail: float
+    right: DevMat | None
+    lam_max: float
+    nkeep: int
+    drift: float
+    reorthed: bool
+    sweeps: int
+    input_count: int
+
+
+def gram_full(parts: list[Part], d: int):
+    """G = D S^T S D for the concatenated (scaled) parts (pod.py:208-211)."""
+    lib = N.load()
+    vs, scale, m, keep = _concat_parts(parts)
+    G = DevMat.empty(m, m)
+    if m:
+        ws = _ws(lib.hp_gram_workspace_bytes(d, m))
+        N.check(lib.hp_gram(vs, d, m, _ptr(scale), G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "gram")
+    return G, m, keep
+
+
+def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
+    """Block Gramian of [Phi*sigma | F] with the diag(sigma^2) top-left block
+    written down (pod.py:376-384)."""
+    lib = N.load()
+    n_old = prior_U.cols
+    vs_f, scale_f, m, keep = _concat_parts(fresh)
+    total = n_old + m
+    G = DevMat.empty(total, total)
+    ws = _ws(lib.hp_block_gram_workspace_bytes(d, n_old, m))
+    N.check(lib.hp_block_gram(prior_U.vecset(), prior_sig_dev.data_ptr(), n_old, vs_f, _ptr(scale_f), m, d,
+                              G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "block gram")
+    return G, total, keep
+
+
+def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
+                       want_right: bool, sqrt_w=None) -> NodeOutput:
+    """pod.py:278-293 on the device: eigensolve, truncation, reconstruction,
+    drift check + re-orthonormalisation, sign convention."""
+    lib = N.load()
+    st = _stream()
+    lam = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
+    V = DevMat.empty(m, m)
+    ws = _ws(lib.hp_syev_workspace_bytes(m))
+    sweeps = ctypes.c_int(0)
+    N.check(lib.hp_syev(G.ptr, G.ld, m, lam.data_ptr(), V.ptr, V.ld, m, JACOBI_TOL_REL, JACOBI_TOL_ABS,
+                        JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ws.data_ptr(), ws.numel(), st), "eigensolve")
+    del ws
+    sig = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
+    info = torch.empty(4, dtype=torch.float64, device="cuda")
+    N.check(lib.hp_truncate(lam.data_ptr(), m, float(eps), float(cutoff), m, sig.data_ptr(), info.data_ptr(), st),
+            "truncate")
+    lam_max, nkeep, n_modes, tail = info.cpu().tolist()
+    nkeep, n_modes = int(nkeep), int(n_modes)
+    if not (lam_max > 0.0):
+        return NodeOutput(None, np.zeros(0), ones(0), 0.0,
+                          DevMat.empty(m, 0) if want_right else None, lam_max, 0, 0.0, False,
+                          sweeps.value, m)
+    sig_dev = sig[:n_modes].clone()
+    if n_modes == 0:
+        return NodeOutput(DevMat.empty(d, 0), np.zeros(0), sig_dev, tail,
+                          DevMat.empty(m, 0) if want_right else None, lam_max, nkeep, 0.0, False,
+                          sweeps.value, m)
+    vs, scale, m2, keep = _concat_parts(parts)
+    assert m2 == m
+    Vn = V.view_cols(0, n_modes)
+    if scale is not None:
+        Vs = DevMat.empty(m, n_modes)
+        N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
+                "scale V")
+    else:
+        Vs = Vn
+    U = DevMat.empty(d, n_modes)
+    ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
+    N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld, ws.data_ptr(),
+                            ws.numel(), st), "assemble")
+    del ws, Vs
+    # drift = max |U^T W U - I| (U is in Euclidean coordinates when weighted)
+    C = DevMat.empty(n_modes, n_modes)
+    drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = _ws(lib.hp_drift_workspace_bytes(d, n_modes))
+    N.check(lib.hp_drift(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
+            "drift")
+    del ws
+    drift = float(drift_dev.item())
+    reorthed = False
+    if drift > DRIFT_TOL:
+        ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
+        passes = ctypes.c_int(0)
+        N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, ctypes.byref(passes),
+                                        ws.data_ptr(), ws.numel(), st), "re-orthonormalisation")
+        del ws
+        reorthed = True
+    del C
+    if sqrt_w is not None:  # back to the space's own coordinates (InnerProductSpace.unweigh)
+        N.check(lib.hp_scale(U.ptr, U.ld, d, n_modes, None, sqrt_w.data_ptr(), None, U.ptr, U.ld, st), "unweigh")
+    R = None
+    if want_right:
+        R = V.view_cols(0, n_modes).clone()
+    N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None, R.ld if R is not None else 0,
+                         m if R is not None else 0, None, st), "signs")
+    sig_host = sig_dev.cpu().numpy()
+    return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps.value, m)
+
+
+def node_pod(parts: list[Part], d: int, eps: float, cutoff: float, want_right: bool, sqrt_w=None) -> NodeOutput:
+    """Full device pod() of the concatenated parts (pod.py:328-337)."""
+    if sqrt_w is not None:
+        parts = weigh_parts(parts, sqrt_w)
+    G, m, _keep = gram_full(parts, d)
+    return spectrum_and_modes(G, m, parts, d, eps, cutoff, want_right, sqrt_w)
+
+
+def node_block_pod(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int, eps: float, cutoff: float,
+                   want_right: bool, sqrt_w=None) -> NodeOutput:
+    """Device block_gramian_pod (pod.py:376-395)."""
+    prior_parts = [Part(prior_U, prior_sig_dev)]
+    if sqrt_w is not None:
+        prior_parts = weigh_parts(prior_parts, sqrt_w)
+        fresh = weigh_parts(fresh, sqrt_w)
+    G, total, _keep = gram_block(prior_parts[0].mat, prior_sig_dev, fresh, d)
+    return spectrum_and_modes(G, total, prior_parts + list(fresh), d, eps, cutoff, want_right, sqrt_w)
+
+
+def synchronize():
+    if D_AVAILABLE():
+        torch.cuda.current_stream().synchronize()
+
+
+def D_AVAILABLE():
+    return torch is not None and torch.cuda.is_available()
+
+
+def residual_energy(S: DevMat, Phi: DevMat | None, sqrt_w=None) -> float:
+    """sum_j ||s_j - Phi Phi^T W s_j||_W^2 with explicit residuals (hierarchy.py:246-253)."""
+    lib = N.load()
+    st = _stream()
+    X = DevMat.empty(S.rows, S.cols)
+    N.check(lib.hp_scale(S.ptr, S.ld, S.rows, S.cols, _ptr(sqrt_w), None, None, X.ptr, X.ld, st), "residual copy")
+    if Phi is not None and Phi.cols:
+        Y = Phi
+        if sqrt_w is not None:
+            Y = DevMat.empty(Phi.rows, Phi.cols)
+            N.check(lib.hp_scale(Phi.ptr, Phi.ld, Phi.rows, Phi.cols, sqrt_w.data_ptr(), None, None, Y.ptr, Y.ld,
+                                 st), "weigh modes")
+        n, m, d = Y.cols, S.cols, S.rows
+        coeff = DevMat.empty(n, m)
+        ws = _ws(max(lib.hp_gemm_workspace_bytes(n, m, d, 0, 0), lib.hp_gemm_workspace_bytes(d, m, n, 0, 0)))
+        N.check(lib.hp_gemm(1, 1, n, m, d, Y.vecset(), X.vecset(), 1.0, 0.0, coeff.ptr, coeff.ld, None, None, None,
+                            0, 0, ws.data_ptr(), ws.numel(), st), "projection coefficients")
+        N.check(lib.hp_gemm(0, 1, d, m, n, Y.vecset(), coeff.vecset(), -1.0, 1.0, X.ptr, X.ld, None, None, None,
+                            0, 0, ws.data_ptr(), ws.numel(), st), "residual")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = _ws(lib.hp_sumsq_workspace_bytes())
+    N.check(lib.hp_sumsq(X.ptr, X.ld, X.rows, X.cols, out.data_ptr(), ws.data_ptr(), ws.numel(), st), "sumsq")
+    return float(out.item())
+
+
+def block_diag_times(blocks: list, right: DevMat) -> DevMat:
+    """stacked_diag(blocks) @ right (hierarchy.py:256-265, 292-295): row block c of
+    the result is blocks[c] @ right[off_c : off_c + cols_c, :]."""
+    lib = N.load()
+    st = _stream()
+    rows = sum(b.rows for b in blocks)
+    ncol = right.cols
+    out = DevMat.empty(rows, ncol, zero=True)
+    r = c = 0
+    for b in blocks:
+        if b.rows and ncol and b.cols:
+            rv = N.VecSet(right.ptr + 8 * c, right.ld, None, int(right.ld % 2 == 0 and (right.ptr + 8 * c) % 16 == 0))
+            tmp = DevMat.empty(b.rows, ncol)
+            ws = _ws(lib.hp_gemm_workspace_bytes(b.rows, ncol, b.cols, 0, 0))
+            N.check(lib.hp_gemm(0, 1, b.rows, ncol, b.cols, b.vecset(), rv, 1.0, 0.0, tmp.ptr, tmp.ld, None, None,
+                                None, 0, 0, ws.data_ptr(), ws.numel(), st), "right factor")
+            N.check(lib.hp_scale(tmp.ptr, tmp.ld, b.rows, ncol, None, None, None, out.ptr + 8 * r, out.ld, st),
+                    "right factor place")
+        r += b.rows
+        c += b.cols
+    return out

@@ -1,0 +1,344 @@
+// extern "C" boundary of libhapod_b200.so (declared in include/hapod_b200.h).
+// Plain pointers and sizes only; every entry returns an hp status code and
+// leaves a thread-local message for hp_last_error().
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+
+#include "hp_common.cuh"
+
+namespace hp {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
+             double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+             const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+size_t syev_workspace_bytes(int64_t n);
+int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, void* ws, size_t ws_bytes,
+             cudaStream_t st);
+int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
+                 cudaStream_t st);
+int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
+int signs_run(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
+              cudaStream_t st);
+int potrf_run(double* A, int64_t lda, int64_t n, double* Dinv, int* info, void* ws, size_t ws_bytes, cudaStream_t st);
+int trtri_run(const double* L, int64_t ldl, int64_t n, const double* Dinv, double* Linv, int64_t ldi, double* T,
+              void* ws, size_t ws_bytes, cudaStream_t st);
+int transpose_run(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd, cudaStream_t st);
+int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* rs, const double* rd,
+              const double* cs, double* dst, int64_t ldd, cudaStream_t st);
+int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st);
+int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, double* partial,
+              cudaStream_t st);
+
+static inline VecSet vs(const hp_vecset& v) { return VecSet{v.base, v.ld, v.table}; }
+
+// ---------------------------------------------------------------- re-orthonormalisation
+struct ReorthoLayout {
+  size_t off_X, off_A, off_Linv, off_Dinv, off_T, off_info, off_gemm, total;
+};
+
+static ReorthoLayout reortho_layout(int64_t d, int64_t N, int64_t ldx) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  ReorthoLayout L;
+  size_t o = 0;
+  const int64_t nblk = (N + 63) / 64;
+  const int64_t ldn = (N + 1) & ~int64_t(1);
+  L.off_X = o;
+  o = al(o + (size_t)ldx * N * 8);
+  L.off_A = o;
+  o = al(o + (size_t)ldn * N * 8);
+  L.off_Linv = o;
+  o = al(o + (size_t)ldn * N * 8);
+  L.off_Dinv = o;
+  o = al(o + (size_t)nblk * 64 * 64 * 8);
+  L.off_T = o;
+  o = al(o + (size_t)64 * std::max<int64_t>(N, 1) * 8);
+  L.off_info = o;
+  o = al(o + 16);
+  L.off_gemm = o;
+  size_t g = std::max(gemm_workspace_bytes(N, N, d, 1, 0), gemm_workspace_bytes(N, N, 64, 1, 0));
+  o = al(o + g);
+  L.total = o;
+  return L;
+}
+
+// One CholQR pass: Y = X * L^{-T} where C = X^T X = L L^T.  C is consumed.
+static int cholqr_pass(const double* X, int64_t ldx, int64_t d, int64_t N, double* C, int64_t ldc, double* Y,
+                       int64_t ldy, const ReorthoLayout& L, char* base, size_t ws_bytes, cudaStream_t st,
+                       int* host_info) {
+  double* Linv = reinterpret_cast<double*>(base + L.off_Linv);
+  double* Dinv = reinterpret_cast<double*>(base + L.off_Dinv);
+  double* T = reinterpret_cast<double*>(base + L.off_T);
+  int* info = reinterpret_cast<int*>(base + L.off_info);
+  void* gws = base + L.off_gemm;
+  const size_t gwsb = ws_bytes - L.off_gemm;
+  const int64_t ldn = (N + 1) & ~int64_t(1);
+  int rc = potrf_run(C, ldc, N, Dinv, info, gws, gwsb, st);
+  if (rc) return rc;
+  HP_CHECK_CUDA(cudaMemcpyAsync(host_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  rc = trtri_run(C, ldc, N, Dinv, Linv, ldn, T, gws, gwsb, st);
+  if (rc) return rc;
+  // Y = X * Linv^T : B(k, n) = Linv(n, k) -> N-major operand (vector k = column k of Linv), upper triangular
+  VecSet a{X, ldx, nullptr};
+  VecSet b{Linv, ldn, nullptr};
+  rc = gemm_run(false, false, d, N, N, a, b, (ldx % 2 == 0) && (ldn % 2 == 0), 1.0, 0.0, Y, ldy, nullptr, nullptr,
+                nullptr, 0, 1, gws, gwsb, st);
+  return rc;
+}
+
+static int gram_sym(const double* X, int64_t ldx, int64_t d, int64_t N, double* C, int64_t ldc, void* ws,
+                    size_t wsb, cudaStream_t st) {
+  VecSet a{X, ldx, nullptr};
+  return gemm_run(true, true, N, N, d, a, a, (ldx % 2 == 0), 1.0, 0.0, C, ldc, nullptr, nullptr, nullptr, 1, 0, ws,
+                  wsb, st);
+}
+
+__global__ void add_diag(double* C, int64_t ldc, int64_t n, double s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) C[i * ldc + i] += s;
+}
+
+__global__ void trace_kernel(const double* C, int64_t ldc, int64_t n, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) s += C[i * ldc + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+__global__ void block_gram_fill(double* G, int64_t ldg, int64_t n_old, int64_t m, const double* sigma) {
+  // top-left diag(sigma^2) (pod.py:377) and the lower-left mirror of the mixed block
+  const int64_t total = n_old + m;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_old * n_old) {
+    const int64_t j = e / n_old, i = e % n_old;
+    G[j * ldg + i] = (i == j) ? sigma[i] * sigma[i] : 0.0;
+  }
+  const int64_t e2 = e - n_old * n_old;
+  if (e2 >= 0 && e2 < n_old * m) {
+    const int64_t j = e2 / m, i = e2 % m;  // lower-left (n_old + i, j) <- upper-right (j, n_old + i)
+    G[j * ldg + n_old + i] = G[(n_old + i) * ldg + j];
+  }
+  (void)total;
+}
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" {
+
+int hp_abi_version(void) { return HP_ABI_VERSION; }
+const char* hp_last_error(void) { return hp::last_error(); }
+
+int hp_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+size_t hp_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
+  return gemm_workspace_bytes(M, N, K, sym, b_upper);
+}
+
+int hp_gemm(int a_kmajor, int b_kmajor, int64_t M, int64_t N, int64_t K, hp_vecset A, hp_vecset B, double alpha,
+            double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+            const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, void* stream) {
+  return gemm_run(a_kmajor != 0, b_kmajor != 0, M, N, K, vs(A), vs(B), A.aligned16 && B.aligned16, alpha, beta, C,
+                  ldc, row_scale, col_scale, col_div, sym, b_upper, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t hp_gram_workspace_bytes(int64_t d, int64_t m) { return gemm_workspace_bytes(m, m, d, 1, 0); }
+
+int hp_gram(hp_vecset S, int64_t d, int64_t m, const double* colscale, double* G, int64_t ldg, void* ws,
+            size_t ws_bytes, void* stream) {
+  HP_REQUIRE(d >= 0 && m >= 0 && ldg >= m, "hp_gram: bad dimensions");
+  return gemm_run(true, true, m, m, d, vs(S), vs(S), S.aligned16 != 0, 1.0, 0.0, G, ldg, colscale, colscale, nullptr,
+                  1, 0, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t hp_block_gram_workspace_bytes(int64_t d, int64_t n_old, int64_t m) {
+  return std::max(gemm_workspace_bytes(n_old, m, d, 0, 0), gemm_workspace_bytes(m, m, d, 1, 0));
+}
+
+int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F, const double* fscale, int64_t m,
+                  int64_t d, double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
+  HP_REQUIRE(n_old >= 0 && m >= 0 && d >= 0 && ldg >= n_old + m, "hp_block_gram: bad dimensions");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m > 0) {
+    // mixed block sigma o (Phi^T F)  (pod.py:379-381)
+    int rc = gemm_run(true, true, n_old, m, d, vs(Phi), vs(F), Phi.aligned16 && F.aligned16, 1.0, 0.0,
+                      G + n_old * ldg, ldg, sigma, fscale, nullptr, 0, 0, ws, ws_bytes, st);
+    if (rc) return rc;
+    // fresh block gramian(F)  (pod.py:383)
+    rc = gemm_run(true, true, m, m, d, vs(F), vs(F), F.aligned16 != 0, 1.0, 0.0, G + n_old * ldg + n_old, ldg,
+                  fscale, fscale, nullptr, 1, 0, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  const int64_t work = n_old * n_old + n_old * m;
+  if (work > 0) {
+    block_gram_fill<<<(unsigned)ceil_div(work, 256), 256, 0, st>>>(G, ldg, n_old, m, sigma);
+    HP_CHECK_LAUNCH("block_gram_fill");
+  }
+  return HP_OK;
+}
+
+size_t hp_syev_workspace_bytes(int64_t n) { return syev_workspace_bytes(n); }
+
+int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, void* ws, size_t ws_bytes, void* stream) {
+  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, max_sweeps, sweeps, ws, ws_bytes,
+                  (cudaStream_t)stream);
+}
+
+int hp_truncate(const double* lam_desc, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info4,
+                void* stream) {
+  HP_REQUIRE(n >= 0 && eps >= 0.0, "hp_truncate: bad arguments");
+  return truncate_run(lam_desc, n, eps, cutoff, m, sigma, info4, (cudaStream_t)stream);
+}
+
+size_t hp_assemble_workspace_bytes(int64_t d, int64_t m, int64_t N) { return gemm_workspace_bytes(d, N, m, 0, 0); }
+
+int hp_assemble(hp_vecset S, int64_t d, int64_t m, const double* V, int64_t ldv, const double* sigma, int64_t N,
+                double* U, int64_t ldu, void* ws, size_t ws_bytes, void* stream) {
+  HP_REQUIRE(N >= 0 && N <= m && ldu >= d && ldv >= m, "hp_assemble: bad dimensions");
+  VecSet b{V, ldv, nullptr};
+  return gemm_run(false, true, d, N, m, vs(S), b, S.aligned16 && (ldv % 2 == 0), 1.0, 0.0, U, ldu, nullptr, nullptr,
+                  sigma, 0, 0, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t hp_drift_workspace_bytes(int64_t d, int64_t N) { return gemm_workspace_bytes(N, N, d, 1, 0); }
+
+int hp_drift(const double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double* drift_out, void* ws,
+             size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = gram_sym(U, ldu, d, N, C, ldc, ws, ws_bytes, st);
+  if (rc) return rc;
+  return drift_run(C, ldc, N, drift_out, st);
+}
+
+size_t hp_reortho_workspace_bytes(int64_t d, int64_t N) {
+  const int64_t ldx = (d + 1) & ~int64_t(1);
+  return reortho_layout(d, N, ldx).total;
+}
+
+// U <- Q of the QR factorisation of U (CholQR2; shifted CholQR3 when the
+// first Cholesky breaks down).  C holds U^T U on entry (from hp_drift) and is
+// destroyed.  Same span and column order as the MGS sweep of pod.py:227-237.
+int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, int* passes_out,
+                        void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (passes_out) *passes_out = 0;
+  if (N == 0) return HP_OK;
+  const int64_t ldx = (d + 1) & ~int64_t(1);
+  const ReorthoLayout L = reortho_layout(d, N, ldx);
+  HP_REQUIRE(ws_bytes >= L.total, "hp_reorthonormalize: workspace too small");
+  char* base = static_cast<char*>(ws);
+  double* X = reinterpret_cast<double*>(base + L.off_X);
+  double* A = reinterpret_cast<double*>(base + L.off_A);
+  const int64_t ldn = (N + 1) & ~int64_t(1);
+  void* gws = base + L.off_gemm;
+  const size_t gwsb = ws_bytes - L.off_gemm;
+  int* hinfo = nullptr;
+  HP_CHECK_CUDA(cudaMallocHost(&hinfo, 2 * sizeof(int)));
+  double* htrace = nullptr;
+  HP_CHECK_CUDA(cudaMallocHost(&htrace, sizeof(double)));
+  int rc = HP_OK;
+  int passes = 0;
+  // keep a copy of C in case the first factorisation fails
+  rc = scale_run(C, ldc, N, N, nullptr, nullptr, nullptr, A, ldn, st);
+  if (!rc) rc = cholqr_pass(U, ldu, d, N, C, ldc, X, ldx, L, base, ws_bytes, st, &hinfo[0]);
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error(std::string("reortho: ") + cudaGetErrorString(e));
+      rc = HP_ECUDA;
+    }
+  }
+  if (!rc && hinfo[0] != 0) {
+    // shifted CholQR (Fukaya et al.): s = 11 (d N + N (N+1)) u ||U||_2^2, ||U||_2^2 <= trace(U^T U)
+    trace_kernel<<<1, 256, 0, st>>>(A, ldn, N, C);
+    cudaMemcpyAsync(htrace, C, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * 1.1102230246251565e-16 * htrace[0];
+    add_diag<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(A, ldn, N, shift);
+    rc = cholqr_pass(U, ldu, d, N, A, ldn, X, ldx, L, base, ws_bytes, st, &hinfo[1]);
+    if (!rc) {
+      cudaStreamSynchronize(st);
+      if (hinfo[1] != 0) {
+        set_error("reortho: shifted Cholesky broke down (modes numerically rank deficient)");
+        rc = HP_ELINALG;
+      }
+    }
+    // bring the shifted result back into U, then two plain passes follow
+    if (!rc) rc = scale_run(X, ldx, d, N, nullptr, nullptr, nullptr, U, ldu, st);
+    if (!rc) rc = gram_sym(U, ldu, d, N, A, ldn, gws, gwsb, st);
+    if (!rc) rc = cholqr_pass(U, ldu, d, N, A, ldn, X, ldx, L, base, ws_bytes, st, &hinfo[0]);
+    passes += 1;
+  }
+  passes += 1;
+  // second pass: X -> U
+  if (!rc) rc = gram_sym(X, ldx, d, N, A, ldn, gws, gwsb, st);
+  if (!rc) rc = cholqr_pass(X, ldx, d, N, A, ldn, U, ldu, L, base, ws_bytes, st, &hinfo[0]);
+  passes += 1;
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error(std::string("reortho: ") + cudaGetErrorString(e));
+      rc = HP_ECUDA;
+    } else if (hinfo[0] != 0) {
+      set_error("reortho: Cholesky of the re-orthonormalised modes broke down");
+      rc = HP_ELINALG;
+    }
+  }
+  cudaFreeHost(hinfo);
+  cudaFreeHost(htrace);
+  if (passes_out) *passes_out = passes;
+  return rc;
+}
+
+int hp_signs(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
+             void* stream) {
+  return signs_run(U, ldu, d, N, R, ldr, mr, sign_out, (cudaStream_t)stream);
+}
+
+int hp_transpose_rm_to_cm(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd, void* stream) {
+  return transpose_run(src, rows, cols, dst, ldd, (cudaStream_t)stream);
+}
+
+int hp_scale(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* row_mul, const double* row_div,
+             const double* col_mul, double* dst, int64_t ldd, void* stream) {
+  return scale_run(src, lds, rows, cols, row_mul, row_div, col_mul, dst, ldd, (cudaStream_t)stream);
+}
+
+int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, void* stream) {
+  return finite_check_run(src, lds, rows, cols, bad, (cudaStream_t)stream);
+}
+
+size_t hp_sumsq_workspace_bytes(void) { return 1024 * sizeof(double); }
+
+int hp_sumsq(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, void* ws, size_t ws_bytes,
+             void* stream) {
+  HP_REQUIRE(ws_bytes >= 1024 * sizeof(double), "hp_sumsq: workspace too small");
+  return sumsq_run(A, lda, rows, cols, out, static_cast<double*>(ws), (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// Shared helpers for the HAPOD B200 kernels (sm_100a).
+//
+// All matrices are float64, column-major.  An "operand" is a set of
+// contiguous vectors addressed either as base + i*ld or through a device
+// table of per-vector pointers (used to read a node's input as the
+// concatenation of its children's mode blocks without an hstack copy,
+// hierarchy.py:284-291).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "hapod_b200.h"
+
+namespace hp {
+
+// thread-local last error message (hp_last_error)
+void set_error(const std::string& msg);
+const char* last_error();
+
+// status codes: enum hp_status of include/hapod_b200.h (HP_OK, HP_EINVAL -> ValueError,
+// HP_ECUDA -> RuntimeError, HP_ELINALG -> LinAlgError, HP_ENOMEM)
+
+#define HP_CHECK_CUDA(expr)                                                          \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::hp::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+      return ::HP_ECUDA;                                                         \
+    }                                                                                \
+  } while (0)
+
+#define HP_CHECK_LAUNCH(what)                                                        \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess) {                                                         \
+      ::hp::set_error(std::string("launch ") + (what) + ": " + cudaGetErrorString(_e)); \
+      return ::HP_ECUDA;                                                         \
+    }                                                                                \
+  } while (0)
+
+#define HP_REQUIRE(cond, msg)                                                        \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      ::hp::set_error(msg);                                                          \
+      return ::HP_EINVAL;                                                        \
+    }                                                                                \
+  } while (0)
+
+// A strided or pointer-table addressed set of vectors.
+struct VecSet {
+  const double* base;          // used when table == nullptr
+  int64_t ld;                  // stride between vectors (elements)
+  const double* const* table;  // optional device table of vector pointers
+  __host__ __device__ __forceinline__ const double* vec(int64_t i) const {
+    return table ? table[i] : base + i * ld;
+  }
+};
+
+// ---------------------------------------------------------------- device PTX
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cp.async with zero fill: copies src_bytes (0..16) and zero-fills the rest.
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms();
+
+}  // namespace hp

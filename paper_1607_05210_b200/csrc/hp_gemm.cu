@@ -1,0 +1,393 @@
+// FP64 DMMA GEMM engine for the HAPOD node contractions (sm_100a).
+//
+//   K1  Gram SYRK      G = S^T S                 (pod.py:208-211, 87-91)   "TN", sym
+//   K1b mixed block    sigma o (Phi^T F)         (pod.py:376-384)          "TN", row scale
+//   K4  reconstruction U = (S V[:, :N]) / sigma  (pod.py:333-334)          "NN", column divide
+//   K5  drift check    U^T U                     (pod.py:245-247)          "TN", sym
+//   CholQR / Cholesky trailing updates                                     "NN" / "NT"
+//
+// FP64 tensor work on sm_100a is warp-level DMMA (mma.sync m8n8k4 f64 ->
+// SASS DMMA.8x8x4); tcgen05 has no f64 kind.  Measured on this pool's B200:
+// DMMA peaks at 37.1 TFLOP/s (tools/microbench/fp64_peak.cu).
+//
+// Tiling: 128x128 CTA tile, 8 warps as 2 (m) x 4 (n), warp tile 64x32 =
+// 8x4 DMMA fragments (64 fp64 accumulators / thread), K tile 16, 4-stage
+// cp.async (LDGSTS) ring with zero-fill at every edge.  The k index is
+// permuted inside a K tile (k = 4t + s when both operands are K-major) so
+// each lane fetches its fragments with 128-bit shared loads; row strides are
+// padded so those loads are bank-conflict free.
+//
+// Operands are VecSets (base+ld or a per-vector pointer table), so a node's
+// input can be the concatenation of its children's mode blocks without an
+// hstack copy.  Split-K over long contractions writes per-split partial tiles
+// that a second kernel sums in a FIXED order: results are bit-identical run to
+// run and independent of how many GPUs take part (no atomics).
+#include <algorithm>
+#include <cmath>
+
+#include "hp_common.cuh"
+
+namespace hp {
+namespace gemm {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+constexpr int LDM = BM + 2;  // [k][m] rows: LD = 2 mod 8 -> conflict-free 128-bit fragment loads
+
+struct Params {
+  int64_t M, N, K;
+  VecSet A, B;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+  const double* row_scale;
+  const double* col_scale;
+  const double* col_div;
+  int sym;
+  int b_upper;
+  int splits;
+  int64_t kspan;
+  double* partial;
+  int tiles_m, tiles_n;
+  int64_t ntiles;
+};
+
+template <bool AK, bool BKM>
+struct Layout {
+  static constexpr bool MODEP = AK && BKM;       // both operands K-major: k = 4t + s
+  static constexpr int LDK = MODEP ? 18 : 20;    // [row][k] stride
+  static constexpr int A_ELEMS = AK ? BM * LDK : BK * LDM;
+  static constexpr int B_ELEMS = BKM ? BN * LDK : BK * LDM;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8;
+};
+
+__device__ __forceinline__ void tile_coords(const Params& p, int64_t t, int& bi, int& bj) {
+  if (p.sym) {
+    // column-major enumeration of the upper triangle: t = bj(bj+1)/2 + bi
+    int j = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(j + 1) * (j + 2) / 2 <= t) ++j;
+    while ((int64_t)j * (j + 1) / 2 > t) --j;
+    bj = j;
+    bi = (int)(t - (int64_t)j * (j + 1) / 2);
+  } else {
+    bi = (int)(t % p.tiles_m);
+    bj = (int)(t / p.tiles_m);
+  }
+}
+
+// Load one operand tile into shared memory.
+//  kmajor: `rows` vectors (m or n) of BK contiguous k's      -> s[row][k]  (LDK)
+//  else  : BK vectors (k) of `rows` contiguous m's (or n's)  -> s[k][row]  (LDM)
+template <bool KMAJOR, bool VEC, int LDK>
+__device__ __forceinline__ void load_operand(double* s, const VecSet& op, int64_t r0, int64_t rlim, int64_t k0,
+                                             int64_t kend, int tid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int c = tid + it * THREADS;
+    int srow, scol;  // smem coordinates
+    int64_t vec_idx, off;
+    int nvalid;
+    if (KMAJOR) {
+      const int row = c >> 3, kc = (c & 7) * 2;
+      const int64_t gr = r0 + row, gk = k0 + kc;
+      vec_idx = gr < rlim ? gr : 0;
+      off = gk;
+      nvalid = gr < rlim ? (int)max((int64_t)0, min((int64_t)2, kend - gk)) : 0;
+      srow = row;
+      scol = kc;
+    } else {
+      const int krow = c >> 6, rc = (c & 63) * 2;
+      const int64_t gk = k0 + krow, gr = r0 + rc;
+      vec_idx = gk < kend ? gk : 0;
+      off = gr;
+      nvalid = gk < kend ? (int)max((int64_t)0, min((int64_t)2, rlim - gr)) : 0;
+      srow = krow;
+      scol = rc;
+    }
+    double* dst = KMAJOR ? s + srow * LDK + scol : s + srow * LDM + scol;
+    const double* vp = op.vec(vec_idx);
+    if (VEC) {
+      const double* src = nvalid ? vp + off : vp;
+      cp_async_16(dst, src, nvalid * 8);
+    } else {
+      cp_async_8(dst, nvalid >= 1 ? vp + off : vp, nvalid >= 1 ? 8 : 0);
+      cp_async_8(dst + 1, nvalid >= 2 ? vp + off + 1 : vp, nvalid >= 2 ? 8 : 0);
+    }
+  }
+}
+
+template <bool AK, bool BKM, bool VEC>
+__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(Params p) {
+  using L = Layout<AK, BKM>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+
+  const int64_t tile = blockIdx.x;
+  const int z = blockIdx.z;
+  int bi, bj;
+  tile_coords(p, tile, bi, bj);
+  const int64_t m0 = (int64_t)bi * BM, n0 = (int64_t)bj * BN;
+
+  const int64_t kbeg = (int64_t)z * p.kspan;
+  int64_t kend = min(p.K, kbeg + p.kspan);
+  if (p.b_upper) kend = min(kend, n0 + BN);
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto stage_a = [&](int s) { return smem + s * L::STAGE_ELEMS; };
+  auto stage_b = [&](int s) { return smem + s * L::STAGE_ELEMS + L::A_ELEMS; };
+  auto load_stage = [&](int s, int64_t k0) {
+    load_operand<AK, VEC, L::LDK>(stage_a(s), p.A, m0, p.M, k0, kend, tid);
+    load_operand<BKM, VEC, L::LDK>(stage_b(s), p.B, n0, p.N, k0, kend, tid);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, kbeg + (int64_t)s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) load_stage(nxt % STAGES, kbeg + (int64_t)nxt * BK);
+    cp_async_commit();
+
+    const double* as = stage_a(kt % STAGES);
+    const double* bs = stage_b(kt % STAGES);
+    if (L::MODEP) {
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp) {
+        double2 af[8], bf[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          af[i] = *reinterpret_cast<const double2*>(as + (wm * 64 + i * 8 + g) * L::LDK + 4 * t + 2 * sp);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          bf[j] = *reinterpret_cast<const double2*>(bs + (wn * 32 + j * 8 + g) * L::LDK + 4 * t + 2 * sp);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
+          }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
+          }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double af[8], bf[4];
+        const int kk = 4 * s + t;
+        if (AK) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) af[i] = as[(wm * 64 + i * 8 + g) * L::LDK + kk];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double2 v = *reinterpret_cast<const double2*>(as + kk * LDM + wm * 64 + g * 8 + 2 * q);
+            af[2 * q] = v.x;
+            af[2 * q + 1] = v.y;
+          }
+        }
+        if (BKM) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bf[j] = bs[(wn * 32 + j * 8 + g) * L::LDK + kk];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double2 v = *reinterpret_cast<const double2*>(bs + kk * LDM + wn * 32 + g * 4 + 2 * q);
+            bf[2 * q] = v.x;
+            bf[2 * q + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---------------------------------------------------------------- epilogue
+  if (p.splits > 1) {
+    double* out = p.partial + ((int64_t)z * p.ntiles + tile) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ml = wm * 64 + (AK ? i * 8 + g : g * 8 + i);
+          const int nl = wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+          out[nl * BM + ml] = acc[i][j][e];
+        }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t m = m0 + wm * 64 + (AK ? i * 8 + g : g * 8 + i);
+        const int64_t n = n0 + wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+        if (m >= p.M || n >= p.N) continue;
+        if (p.sym && m > n) continue;
+        double v = p.alpha * acc[i][j][e];
+        if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
+        if (p.row_scale) v *= p.row_scale[m];
+        if (p.col_scale) v *= p.col_scale[n];
+        if (p.col_div) v /= p.col_div[n];
+        p.C[n * p.ldc + m] = v;
+        if (p.sym && m != n) p.C[m * p.ldc + n] = v;
+      }
+}
+
+// Fixed-order split-K reduction + epilogue.  One thread per tile element.
+__global__ void splitk_reduce(Params p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tile = idx / (BM * BN);
+  if (tile >= p.ntiles) return;
+  const int e = (int)(idx % (BM * BN));
+  const int nl = e / BM, ml = e % BM;
+  int bi, bj;
+  tile_coords(p, tile, bi, bj);
+  const int64_t m = (int64_t)bi * BM + ml, n = (int64_t)bj * BN + nl;
+  if (m >= p.M || n >= p.N) return;
+  if (p.sym && m > n) return;
+  double s = 0.0;
+  for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * p.ntiles + tile) * (BM * BN) + e];
+  double v = p.alpha * s;
+  if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
+  if (p.row_scale) v *= p.row_scale[m];
+  if (p.col_scale) v *= p.col_scale[n];
+  if (p.col_div) v /= p.col_div[n];
+  p.C[n * p.ldc + m] = v;
+  if (p.sym && m != n) p.C[m * p.ldc + n] = v;
+}
+
+struct Plan {
+  int tiles_m, tiles_n;
+  int64_t ntiles;
+  int splits;
+  int64_t kspan;
+  size_t ws_bytes;
+};
+
+Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
+  Plan pl;
+  pl.tiles_m = (int)ceil_div(M, BM);
+  pl.tiles_n = (int)ceil_div(N, BN);
+  pl.ntiles = sym ? (int64_t)pl.tiles_m * (pl.tiles_m + 1) / 2 : (int64_t)pl.tiles_m * pl.tiles_n;
+  // Split-K only when the output alone cannot fill the chip.  Depends on the
+  // shape only (never on the device count) so results are reproducible.
+  const int64_t target = 2 * 148;
+  int64_t splits = 1;
+  if (!b_upper && pl.ntiles < target) {
+    splits = target / std::max<int64_t>(pl.ntiles, 1);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(K / 512, 1));  // >= 512 k per split
+    splits = std::min<int64_t>(splits, 64);
+    splits = std::max<int64_t>(splits, 1);
+  }
+  pl.kspan = ceil_div(ceil_div(K, splits), BK) * BK;
+  splits = std::max<int64_t>(1, ceil_div(K, std::max<int64_t>(pl.kspan, 1)));
+  pl.splits = (int)splits;
+  pl.ws_bytes = pl.splits > 1 ? (size_t)pl.splits * pl.ntiles * BM * BN * sizeof(double) : 0;
+  return pl;
+}
+
+template <bool AK, bool BKM, bool VEC>
+int launch_t(const Params& p, cudaStream_t st) {
+  using L = Layout<AK, BKM>;
+  static bool configured = false;
+  if (!configured) {
+    HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_kernel<AK, BKM, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       L::SMEM_BYTES));
+    configured = true;
+  }
+  dim3 grid((unsigned)p.ntiles, 1, (unsigned)p.splits);
+  gemm_kernel<AK, BKM, VEC><<<grid, THREADS, L::SMEM_BYTES, st>>>(p);
+  HP_CHECK_LAUNCH("gemm_kernel");
+  return HP_OK;
+}
+
+}  // namespace gemm
+
+// Host entry used by the C-ABI and by the other modules.
+int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
+             double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+             const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace gemm;
+  HP_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: negative dimension");
+  HP_REQUIRE(!sym || M == N, "gemm: symmetric output needs M == N");
+  HP_REQUIRE(!(a_kmajor == false && b_kmajor == false) || true, "");
+  if (M == 0 || N == 0) return HP_OK;
+  Params p{};
+  Plan pl = make_plan(M, N, K, sym, b_upper);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.ldc = ldc;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.row_scale = row_scale;
+  p.col_scale = col_scale;
+  p.col_div = col_div;
+  p.sym = sym;
+  p.b_upper = b_upper;
+  p.tiles_m = pl.tiles_m;
+  p.tiles_n = pl.tiles_n;
+  p.ntiles = pl.ntiles;
+  p.splits = pl.splits;
+  p.kspan = pl.kspan;
+  if (pl.splits > 1) {
+    if (ws_bytes < pl.ws_bytes) {
+      // not enough workspace: fall back to a single split (same arithmetic class, one more wave)
+      p.splits = 1;
+      p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
+    } else {
+      p.partial = static_cast<double*>(ws);
+    }
+  }
+  int rc;
+  if (a_kmajor && b_kmajor)
+    rc = aligned16 ? launch_t<true, true, true>(p, st) : launch_t<true, true, false>(p, st);
+  else if (!a_kmajor && b_kmajor)
+    rc = aligned16 ? launch_t<false, true, true>(p, st) : launch_t<false, true, false>(p, st);
+  else if (!a_kmajor && !b_kmajor)
+    rc = aligned16 ? launch_t<false, false, true>(p, st) : launch_t<false, false, false>(p, st);
+  else
+    rc = aligned16 ? launch_t<true, false, true>(p, st) : launch_t<true, false, false>(p, st);
+  if (rc) return rc;
+  if (p.splits > 1) {
+    const int64_t total = p.ntiles * BM * BN;
+    splitk_reduce<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(p);
+    HP_CHECK_LAUNCH("splitk_reduce");
+  }
+  return HP_OK;
+}
+
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
+  if (M <= 0 || N <= 0) return 0;
+  return gemm::make_plan(M, N, K, sym, b_upper).ws_bytes;
+}
+
+}  // namespace hp

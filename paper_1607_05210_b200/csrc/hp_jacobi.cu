@@ -1,0 +1,585 @@
+// K2: symmetric eigensolve of the node Gramian by two-sided parallel block
+// Jacobi (replaces scipy.linalg.eigh / LAPACK dsyevr, pod.py:329-331,386-388).
+//
+// The padded n_p x n_p matrix (n_p = nb*32, nb even) is split into nb block
+// columns of width 32.  A sweep is nb-1 rounds of a round-robin tournament;
+// in each round the nb/2 disjoint block pairs (p,q) are processed at once:
+//
+//   jac_local : one CTA per pair loads the 64x64 sub-problem G[I,I],
+//               I = block p U block q, into shared memory.  If any off-diagonal
+//               entry exceeds tol_abs * max|g_ii| it diagonalises the copy with
+//               cyclic parallel-order Jacobi (32 disjoint rotations per step,
+//               63 steps per local sweep, relative threshold
+//               |a_ij| > tol_rel sqrt|a_ii a_jj|) while accumulating the 64x64
+//               rotation W, then re-orthonormalises W with one Bjorck step
+//               (W += W (I - W^T W) / 2).  Only W is written.
+//   jac_apply : G <- J^T G J and V <- V J for the block-diagonal J built from
+//               the W's, as 64x64x64 DMMA products in shared memory: one CTA
+//               per upper 64x64 tile pair of G (the pair's own diagonal tile
+//               included) and per 64-row slab of V.  Every tile sees the same
+//               orthonormal W, so each round is a similarity transform up to
+//               GEMM rounding -- the backward error stays at the u*||G|| level
+//               instead of growing with the number of rotations.
+//
+// A sweep in which no pair needed work ends the iteration; a sweep whose
+// largest off-diagonal ratio no longer halves while sitting at the rounding
+// floor (< 512 u) is accepted as converged as well.  Eigenvalues are then the
+// Rayleigh quotients v^T G0 v / v^T v against the ORIGINAL Gramian, sorted
+// descending (ties by index), with V's columns permuted to match -- the
+// "eigh then reverse" order of pod.py:329-331.
+// Padding rows/columns are exactly zero and are never rotated against real
+// indices (their off-diagonal entries stay exactly 0), so they are dropped
+// by index at the end.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "hp_common.cuh"
+
+namespace hp {
+int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
+             double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+             const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+namespace jac {
+
+constexpr int BW = 32;        // block width
+constexpr int PS = 2 * BW;    // local problem size
+constexpr int LS = PS + 1;    // local smem stride
+constexpr int LT = 256;       // local solver threads
+constexpr int TS = PS + 4;    // apply-kernel smem stride (= 4 mod 16: conflict-free DMMA fragments)
+constexpr int AT = 256;       // apply threads
+
+struct Params {
+  double* G;          // n_p x n_p, ld = n_p
+  double* V;          // n_p x n_p, ld = n_p
+  int64_t np;
+  int nb;             // number of 32-wide blocks (even)
+  int round;
+  double* W;          // (nb/2) x 64 x 64, col-major per pair
+  int* flags;         // nb/2
+  int* counter;       // pairs that needed work in this sweep
+  double* maxoff;     // max |g_ij| / max|g_ii| seen in this sweep (atomic max on the bit pattern)
+  const double* scal; // scal[0] = max |g_ii| of the input
+  double tol_rel, tol_abs;
+  int max_local_sweeps;
+};
+
+__device__ __forceinline__ void circle_pair(int nplayers, int r, int k, int& a, int& b) {
+  // round-robin "circle method": player nplayers-1 fixed, others rotate
+  const int m = nplayers - 1;
+  if (k == 0) {
+    a = m;
+    b = r % m;
+  } else {
+    a = (r + k) % m;
+    b = (r - k + m) % m;
+  }
+}
+
+__device__ __forceinline__ void block_pair(const Params& p, int k, int& bp, int& bq) {
+  int a, b;
+  circle_pair(p.nb, p.round, k, a, b);
+  bp = min(a, b);
+  bq = max(a, b);
+}
+
+__device__ __forceinline__ int64_t local_index(int bp, int bq, int i) {
+  return i < BW ? (int64_t)bp * BW + i : (int64_t)bq * BW + (i - BW);
+}
+
+__device__ __forceinline__ bool needs_rotation(double aij, double aii, double ajj, double tr, double ta) {
+  const double a = fabs(aij);
+  return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj));
+}
+
+__global__ void __launch_bounds__(LT) jac_local(Params p) {
+  extern __shared__ double sm[];
+  double* A = sm;               // PS x LS (A[i*LS + j] = a_ij, symmetric)
+  double* Wl = A + PS * LS;     // PS x LS (Wl[i*LS + j] = w_ij)
+  __shared__ double cs[PS / 2], sn[PS / 2], tt[PS / 2];
+  __shared__ int pi[PS / 2], pj[PS / 2], rot[PS / 2];
+  __shared__ int any_rot;
+
+  const int k = blockIdx.x;
+  int bp, bq;
+  block_pair(p, k, bp, bq);
+  const int tid = threadIdx.x;
+  const double tr = p.tol_rel, ta = p.tol_abs * p.scal[0];
+
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int j = e / PS, i = e % PS;
+    A[i * LS + j] = p.G[local_index(bp, bq, j) * p.np + local_index(bp, bq, i)];
+  }
+  __syncthreads();
+  // anything to do?  (absolute trigger: tol_abs * max|g_ii|)
+  int mine = 0;
+  double moff = 0.0;
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int i = e / PS, j = e % PS;
+    if (i < j) {
+      const double a = fabs(A[i * LS + j]);
+      moff = fmax(moff, a);
+      if (a > ta) mine = 1;
+    }
+  }
+  {
+    // sweep-level maximum off-diagonal ratio (non-negative doubles order like their bits)
+    double r = moff / p.scal[0];
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if ((tid & 31) == 0 && r > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(p.maxoff), (unsigned long long)__double_as_longlong(r));
+  }
+  if (!__syncthreads_or(mine)) {
+    if (tid == 0) p.flags[k] = 0;
+    return;
+  }
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int i = e / PS, j = e % PS;
+    Wl[i * LS + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  for (int sweep = 0; sweep < p.max_local_sweeps; ++sweep) {
+    if (tid == 0) any_rot = 0;
+    __syncthreads();
+    for (int step = 0; step < PS - 1; ++step) {
+      if (tid < PS / 2) {
+        int a, b;
+        circle_pair(PS, step, tid, a, b);
+        const double aii = A[a * LS + a], ajj = A[b * LS + b], aij = A[a * LS + b];
+        int r = needs_rotation(aij, aii, ajj, tr, 1e-300 * p.scal[0]);
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (r) {
+          const double theta = (ajj - aii) / (2.0 * aij);
+          if (fabs(theta) > 1e150) {
+            t = 0.5 / theta;
+          } else {
+            t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          }
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          any_rot = 1;
+        }
+        cs[tid] = c;
+        sn[tid] = s;
+        tt[tid] = t;
+        pi[tid] = a;
+        pj[tid] = b;
+        rot[tid] = r;
+      }
+      __syncthreads();
+      // A <- R^T A R, one 2x2 block per (row pair, column pair)
+      for (int e = tid; e < (PS / 2) * (PS / 2); e += LT) {
+        const int P = e / (PS / 2), Q = e % (PS / 2);
+        const int rp = rot[P], rq = rot[Q];
+        if (!rp && !rq) continue;
+        const int i1 = pi[P], j1 = pj[P], i2 = pi[Q], j2 = pj[Q];
+        if (P == Q) {
+          const double aij = A[i1 * LS + j1];
+          const double t = tt[P];
+          A[i1 * LS + i1] -= t * aij;
+          A[j1 * LS + j1] += t * aij;
+          A[i1 * LS + j1] = 0.0;
+          A[j1 * LS + i1] = 0.0;
+          continue;
+        }
+        double b00 = A[i1 * LS + i2], b01 = A[i1 * LS + j2], b10 = A[j1 * LS + i2], b11 = A[j1 * LS + j2];
+        if (rp) {
+          const double c = cs[P], s = sn[P];
+          const double n00 = c * b00 - s * b10, n01 = c * b01 - s * b11;
+          const double n10 = s * b00 + c * b10, n11 = s * b01 + c * b11;
+          b00 = n00;
+          b01 = n01;
+          b10 = n10;
+          b11 = n11;
+        }
+        if (rq) {
+          const double c = cs[Q], s = sn[Q];
+          const double n00 = c * b00 - s * b01, n01 = s * b00 + c * b01;
+          const double n10 = c * b10 - s * b11, n11 = s * b10 + c * b11;
+          b00 = n00;
+          b01 = n01;
+          b10 = n10;
+          b11 = n11;
+        }
+        A[i1 * LS + i2] = b00;
+        A[i1 * LS + j2] = b01;
+        A[j1 * LS + i2] = b10;
+        A[j1 * LS + j2] = b11;
+      }
+      // W <- W R
+      for (int e = tid; e < PS * (PS / 2); e += LT) {
+        const int r = e / (PS / 2), Q = e % (PS / 2);
+        if (!rot[Q]) continue;
+        const int i2 = pi[Q], j2 = pj[Q];
+        const double c = cs[Q], s = sn[Q];
+        const double wi = Wl[r * LS + i2], wj = Wl[r * LS + j2];
+        Wl[r * LS + i2] = c * wi - s * wj;
+        Wl[r * LS + j2] = s * wi + c * wj;
+      }
+      __syncthreads();
+    }
+    if (!any_rot) break;
+  }
+  // one Bjorck step: E = I - W^T W ; W <- W + W E / 2   (result staged in A's buffer)
+  double* E = Wl + PS * LS;
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int i = e / PS, j = e % PS;
+    double sdot = 0.0;
+    for (int q = 0; q < PS; ++q) sdot += Wl[q * LS + i] * Wl[q * LS + j];
+    E[i * LS + j] = (i == j ? 1.0 : 0.0) - sdot;
+  }
+  __syncthreads();
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int r = e / PS, j = e % PS;
+    double sdot = 0.0;
+    for (int q = 0; q < PS; ++q) sdot += Wl[r * LS + q] * E[q * LS + j];
+    A[r * LS + j] = Wl[r * LS + j] + 0.5 * sdot;
+  }
+  __syncthreads();
+  for (int e = tid; e < PS * PS; e += LT) {
+    const int j = e / PS, i = e % PS;
+    p.W[(int64_t)k * PS * PS + j * PS + i] = A[i * LS + j];
+  }
+  if (tid == 0) {
+    p.flags[k] = 1;
+    atomicAdd(p.counter, 1);
+  }
+}
+
+// C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
+//  transX = false: X(m,k) at X[k*TS + m];  transX = true: X(m,k) = X[m*TS + k]
+// 8 warps: warp w owns rows (w&3)*16..+16 and cols (w>>2)*32..+32.
+template <bool TRANSX>
+__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&acc)[2][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < PS; k0 += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int m = r0 + i * 8 + g, kk = k0 + t;
+      a[i] = TRANSX ? X[m * TS + kk] : X[kk * TS + m];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Y[(c0 + j * 8 + g) * TS + k0 + t];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+  }
+}
+
+__device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C[(c0 + j * 8 + 2 * t + e) * TS + r0 + i * 8 + g] = acc[i][j][e];
+}
+
+__device__ __forceinline__ void load_w(double* dst, const double* W) {
+  for (int e = threadIdx.x; e < PS * PS; e += AT) {
+    const int j = e / PS, i = e % PS;
+    dst[j * TS + i] = W[e];
+  }
+}
+
+__global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
+  extern __shared__ double sm[];
+  double* X = sm;
+  double* WQ = X + PS * TS;
+  double* WP = WQ + PS * TS;
+  const int npairs = p.nb / 2;
+  const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
+  const int64_t b = blockIdx.x;
+  double acc[2][4][2];
+  if (b < ng) {
+    // G tile (P, Q), P <= Q: column-major enumeration of the upper triangle, b = Q(Q+1)/2 + P
+    int Q = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(Q + 1) * (Q + 2) / 2 <= b) ++Q;
+    while ((int64_t)Q * (Q + 1) / 2 > b) --Q;
+    const int P = (int)(b - (int64_t)Q * (Q + 1) / 2);
+    const int fP = p.flags[P], fQ = p.flags[Q];
+    if (!fP && !fQ) return;
+    int pp, pq, qp, qq;
+    block_pair(p, P, pp, pq);
+    block_pair(p, Q, qp, qq);
+    for (int e = threadIdx.x; e < PS * PS; e += AT) {
+      const int j = e / PS, i = e % PS;
+      X[j * TS + i] = p.G[local_index(qp, qq, j) * p.np + local_index(pp, pq, i)];
+    }
+    if (fQ) load_w(WQ, p.W + (int64_t)Q * PS * PS);
+    if (fP) load_w(WP, p.W + (int64_t)P * PS * PS);
+    __syncthreads();
+    if (fQ) {
+      mm64<false>(X, WQ, acc);  // X W_Q
+      __syncthreads();
+      store_acc(X, acc);
+      __syncthreads();
+    }
+    if (fP) {
+      mm64<true>(WP, X, acc);   // W_P^T X
+      __syncthreads();
+      store_acc(X, acc);
+      __syncthreads();
+    }
+    if (P == Q) {
+      // diagonal tile: keep G exactly symmetric (upper triangle mirrored)
+      for (int e = threadIdx.x; e < PS * PS; e += AT) {
+        const int j = e / PS, i = e % PS;
+        const double v = i <= j ? X[j * TS + i] : X[i * TS + j];
+        p.G[local_index(pp, pq, j) * p.np + local_index(pp, pq, i)] = v;
+      }
+      return;
+    }
+    for (int e = threadIdx.x; e < PS * PS; e += AT) {
+      const int j = e / PS, i = e % PS;
+      p.G[local_index(qp, qq, j) * p.np + local_index(pp, pq, i)] = X[j * TS + i];
+    }
+    for (int e = threadIdx.x; e < PS * PS; e += AT) {
+      const int i = e / PS, j = e % PS;
+      p.G[local_index(pp, pq, i) * p.np + local_index(qp, qq, j)] = X[j * TS + i];
+    }
+    return;
+  }
+  // V slab: rows [rc*64, rc*64+64), columns of pair Q
+  const int64_t vb = b - ng;
+  const int Q = (int)(vb % npairs);
+  const int64_t rc = vb / npairs;
+  if (!p.flags[Q]) return;
+  int qp, qq;
+  block_pair(p, Q, qp, qq);
+  for (int e = threadIdx.x; e < PS * PS; e += AT) {
+    const int j = e / PS, i = e % PS;
+    X[j * TS + i] = p.V[local_index(qp, qq, j) * p.np + rc * PS + i];
+  }
+  load_w(WQ, p.W + (int64_t)Q * PS * PS);
+  __syncthreads();
+  mm64<false>(X, WQ, acc);
+  __syncthreads();
+  store_acc(X, acc);
+  __syncthreads();
+  for (int e = threadIdx.x; e < PS * PS; e += AT) {
+    const int j = e / PS, i = e % PS;
+    p.V[local_index(qp, qq, j) * p.np + rc * PS + i] = X[j * TS + i];
+  }
+}
+
+__global__ void pad_copy(const double* G, int64_t ldg, int64_t n, double* Gp, double* Vp, int64_t np) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= np * np) return;
+  const int64_t j = e / np, i = e % np;
+  Gp[e] = (i < n && j < n) ? G[j * ldg + i] : 0.0;
+  Vp[e] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void max_abs_diag(const double* Gp, int64_t np, int64_t n, double* out) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(Gp[i * np + i]));
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0] > 0.0 ? red[0] : 1.0;
+}
+
+// Rayleigh quotients against the ORIGINAL Gramian: rq_i = v_i^T (G0 v_i), one
+// warp per column, fixed summation order (deterministic).  Removes the
+// eigenvalue drift that the accumulated local rotations leave in diag(G).
+__global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t ldy, int64_t n, double* out) {
+  const int64_t col = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (col >= n) return;
+  double s = 0.0, nn = 0.0;
+  for (int64_t k = lane; k < n; k += 32) {
+    const double v = V[col * ldv + k];
+    s += v * Y[col * ldy + k];
+    nn += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    nn += __shfl_xor_sync(0xffffffffu, nn, o);
+  }
+  if (lane == 0) out[col] = s / nn;
+}
+
+// rank of each value in descending order, ties broken by index
+__global__ void sort_rank(const double* dvals, int64_t n, double* lam, int* perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = dvals[i];
+  int64_t r = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const double dj = dvals[j];
+    r += (dj > di) || (dj == di && j < i);
+  }
+  lam[r] = di;
+  perm[r] = (int)i;
+}
+
+__global__ void gather_vectors(const double* Vp, int64_t np, int64_t n, const int* perm, int64_t nvec, double* V,
+                               int64_t ldv) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * nvec) return;
+  const int64_t k = e / n, i = e % n;
+  V[k * ldv + i] = Vp[(int64_t)perm[k] * np + i];
+}
+
+struct Layout {
+  int64_t np;
+  int nb;
+  size_t off_G, off_V, off_W, off_flags, off_counter, off_scal, off_perm, off_rq, off_gemm, total;
+};
+
+Layout layout(int64_t n) {
+  Layout L;
+  int nb = (int)ceil_div(std::max<int64_t>(n, 1), BW);
+  if (nb < 2) nb = 2;
+  if (nb & 1) ++nb;
+  L.nb = nb;
+  L.np = (int64_t)nb * BW;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t o = 0;
+  L.off_G = o;
+  o = al(o + (size_t)L.np * L.np * 8);
+  L.off_V = o;
+  o = al(o + (size_t)L.np * L.np * 8);
+  L.off_W = o;
+  o = al(o + (size_t)(nb / 2) * PS * PS * 8);
+  L.off_flags = o;
+  o = al(o + (size_t)(nb / 2) * 4);
+  L.off_counter = o;
+  o = al(o + 32);
+  L.off_scal = o;
+  o = al(o + 16);
+  L.off_perm = o;
+  o = al(o + (size_t)std::max<int64_t>(n, 1) * 4);
+  L.off_rq = o;
+  o = al(o + (size_t)std::max<int64_t>(n, 1) * 8);
+  L.off_gemm = o;
+  o = al(o + gemm_workspace_bytes(n, n, n, 0, 0));
+  L.total = o;
+  return L;
+}
+
+}  // namespace jac
+
+size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
+
+int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+  using namespace jac;
+  HP_REQUIRE(n >= 0, "syev: negative order");
+  if (sweeps_out) *sweeps_out = 0;
+  if (n == 0) return HP_OK;
+  HP_REQUIRE(ldg >= n && ldv >= n, "syev: leading dimension too small");
+  HP_REQUIRE(nvec >= 0 && nvec <= n, "syev: nvec out of range");
+  const Layout L = layout(n);
+  HP_REQUIRE(ws_bytes >= L.total, "syev: workspace too small");
+  char* base = static_cast<char*>(ws);
+  Params p{};
+  p.G = reinterpret_cast<double*>(base + L.off_G);
+  p.V = reinterpret_cast<double*>(base + L.off_V);
+  p.W = reinterpret_cast<double*>(base + L.off_W);
+  p.flags = reinterpret_cast<int*>(base + L.off_flags);
+  p.counter = reinterpret_cast<int*>(base + L.off_counter);
+  p.maxoff = reinterpret_cast<double*>(base + L.off_counter + 16);
+  double* scal = reinterpret_cast<double*>(base + L.off_scal);
+  p.scal = scal;
+  int* perm = reinterpret_cast<int*>(base + L.off_perm);
+  p.np = L.np;
+  p.nb = L.nb;
+  p.tol_rel = tol_rel;
+  p.tol_abs = tol_abs;
+  p.max_local_sweeps = 40;
+
+  static bool configured = false;
+  const int local_smem = 3 * PS * LS * 8;
+  const int apply_smem = 3 * PS * TS * 8;
+  if (!configured) {
+    HP_CHECK_CUDA(cudaFuncSetAttribute(jac_local, cudaFuncAttributeMaxDynamicSharedMemorySize, local_smem));
+    HP_CHECK_CUDA(cudaFuncSetAttribute(jac_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem));
+    configured = true;
+  }
+  const int64_t npn = L.np * L.np;
+  pad_copy<<<(unsigned)ceil_div(npn, 256), 256, 0, st>>>(G, ldg, n, p.G, p.V, L.np);
+  HP_CHECK_LAUNCH("pad_copy");
+  max_abs_diag<<<1, 256, 0, st>>>(p.G, L.np, n, scal);
+  HP_CHECK_LAUNCH("max_abs_diag");
+
+  const int npairs = L.nb / 2;
+  const int64_t napply = (int64_t)npairs * (npairs + 1) / 2 + (L.np / PS) * npairs;
+  char* host_buf = nullptr;
+  HP_CHECK_CUDA(cudaMallocHost(&host_buf, 32));
+  int status = HP_ELINALG;
+  int sweep = 0;
+  double prev_off = INFINITY;
+  const double floor_ratio = 512.0 * 2.220446049250313e-16;
+  for (; sweep < max_sweeps; ++sweep) {
+    cudaError_t e = cudaMemsetAsync(p.counter, 0, 32, st);
+    if (e != cudaSuccess) break;
+    for (int r = 0; r < L.nb - 1; ++r) {
+      p.round = r;
+      jac_local<<<npairs, LT, local_smem, st>>>(p);
+      jac_apply<<<(unsigned)napply, AT, apply_smem, st>>>(p);
+    }
+    e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      cudaFreeHost(host_buf);
+      set_error(std::string("syev sweep: ") + cudaGetErrorString(e));
+      return HP_ECUDA;
+    }
+    const int worked = *reinterpret_cast<int*>(host_buf);
+    const double off = *reinterpret_cast<double*>(host_buf + 16);
+    if (worked == 0 || (off < floor_ratio && off > 0.5 * prev_off)) {
+      status = HP_OK;
+      break;
+    }
+    prev_off = off;
+  }
+  cudaFreeHost(host_buf);
+  if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
+  if (status != HP_OK) {
+    set_error("syev: Jacobi iteration did not converge");
+    return HP_ELINALG;
+  }
+  // Rayleigh-quotient refinement: Y = G0 V (Y reuses the padded G buffer), rq_i = v_i . y_i
+  {
+    VecSet a{G, ldg, nullptr};
+    VecSet b{p.V, L.np, nullptr};
+    const bool al16 = (ldg % 2 == 0) && ((uintptr_t)G % 16 == 0);
+    int rc = gemm_run(false, true, n, n, n, a, b, al16, 1.0, 0.0, p.G, L.np, nullptr, nullptr, nullptr, 0, 0,
+                      base + L.off_gemm, L.total - L.off_gemm, st);
+    if (rc) return rc;
+    double* rq = reinterpret_cast<double*>(base + L.off_rq);
+    rq_diag<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, rq);
+    HP_CHECK_LAUNCH("rq_diag");
+    sort_rank<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(rq, n, lam_desc, perm);
+    HP_CHECK_LAUNCH("sort_rank");
+  }
+  if (nvec > 0) {
+    gather_vectors<<<(unsigned)ceil_div(n * nvec, 256), 256, 0, st>>>(p.V, L.np, n, perm, nvec, V, ldv);
+    HP_CHECK_LAUNCH("gather_vectors");
+  }
+  return HP_OK;
+}
+
+}  // namespace hp

@@ -1,0 +1,444 @@
+// Per-node POD steps around the contractions:
+//   K3 truncation scan   (pod.py:190-205, 278-289)
+//   K5 drift reduction   (pod.py:245-247) + CholQR re-orthonormalisation
+//      (same span and Gram-Schmidt order as the MGS sweep of pod.py:227-237)
+//   K6 sign convention   (pod.py:214-224)
+// plus layout helpers (row-major upload transpose, sqrt(w) row scaling for
+// weighted spaces pod.py:76-84, column scaling for ModeSet.scaled pod.py:160-162).
+#include <algorithm>
+#include <cmath>
+
+#include "hp_common.cuh"
+
+namespace hp {
+
+int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
+             double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+             const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+
+// ------------------------------------------------------------------ K3 truncation
+// info[0] = lam_max, info[1] = nkeep, info[2] = N, info[3] = tail_energy
+constexpr int TR_T = 1024;
+
+__global__ void __launch_bounds__(TR_T) truncate_kernel(const double* lam, int64_t n, double eps, double cutoff,
+                                                        int64_t m, double* sigma, double* info) {
+  __shared__ double chunk_tot[TR_T];
+  __shared__ double chunk_off[TR_T];
+  __shared__ int64_t sh_nkeep, sh_N;
+  __shared__ double red[TR_T];
+  const int tid = threadIdx.x;
+  const double lam_max = n > 0 ? lam[0] : 0.0;
+  if (!(lam_max > 0.0)) {
+    if (tid == 0) {
+      info[0] = lam_max;
+      info[1] = 0;
+      info[2] = 0;
+      info[3] = 0.0;
+    }
+    return;
+  }
+  const double thr = cutoff * lam_max * (double)m;
+  if (tid == 0) {
+    sh_nkeep = 0;
+    sh_N = n;  // placeholder
+  }
+  __syncthreads();
+  // keep = lam >= thr  (a prefix, lam sorted descending)
+  int64_t local_cnt = 0;
+  for (int64_t i = tid; i < n; i += TR_T) local_cnt += (lam[i] >= thr);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&sh_nkeep), (unsigned long long)local_cnt);
+  __syncthreads();
+  const int64_t nk = sh_nkeep;
+  for (int64_t i = tid; i < nk; i += TR_T) sigma[i] = sqrt(lam[i]);
+  // tails[k] = sum_{i>=k} sigma_i^2, accumulated from the smallest upward within
+  // contiguous chunks, chunk offsets accumulated from the last chunk backward
+  const int64_t cs = (nk + TR_T - 1) / TR_T;
+  const int64_t b = (int64_t)tid * cs, e = min(nk, b + cs);
+  double s = 0.0;
+  for (int64_t i = e - 1; i >= b; --i) {
+    const double si = sqrt(lam[i]);
+    s += si * si;
+  }
+  chunk_tot[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double acc = 0.0;
+    for (int c = TR_T - 1; c >= 0; --c) {
+      chunk_off[c] = acc;
+      acc += chunk_tot[c];
+    }
+    sh_N = nk;  // tails[nk] = 0 always satisfies the budget
+  }
+  __syncthreads();
+  const double eps2 = eps * eps;
+  double run = chunk_off[tid];
+  int64_t first = nk;
+  for (int64_t i = e - 1; i >= b; --i) {
+    const double si = sqrt(lam[i]);
+    run += si * si;
+    if (run <= eps2) first = i;  // tails are non-increasing in i: keep the smallest index
+  }
+  if (first < nk) atomicMin(reinterpret_cast<unsigned long long*>(&sh_N), (unsigned long long)first);
+  __syncthreads();
+  const int64_t N = sh_N;
+  // tail energy = sum lam[N:nk]
+  double t = 0.0;
+  for (int64_t i = N + tid; i < nk; i += TR_T) t += lam[i];
+  red[tid] = t;
+  __syncthreads();
+  for (int st = TR_T / 2; st > 0; st >>= 1) {
+    if (tid < st) red[tid] += red[tid + st];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    info[0] = lam_max;
+    info[1] = (double)nk;
+    info[2] = (double)N;
+    info[3] = red[0];
+  }
+}
+
+int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
+                 cudaStream_t st) {
+  truncate_kernel<<<1, TR_T, 0, st>>>(lam, n, eps, cutoff, m, sigma, info);
+  HP_CHECK_LAUNCH("truncate_kernel");
+  return HP_OK;
+}
+
+// ------------------------------------------------------------------ K5 drift
+__device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
+  // non-negative doubles order like their bit patterns
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void drift_kernel(const double* C, int64_t ldc, int64_t n, double* out) {
+  __shared__ double red[256];
+  double mx = 0.0;
+  const int64_t total = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    double v = C[j * ldc + i] - (i == j ? 1.0 : 0.0);
+    v = fabs(v);
+    if (!(v <= mx)) mx = v;  // propagates NaN as +inf-ish below
+  }
+  if (mx != mx) mx = INFINITY;
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomic_max_pos(out, red[0]);
+}
+
+int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st) {
+  HP_CHECK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  if (n == 0) return HP_OK;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n * n, 256), 4 * 148);
+  drift_kernel<<<(unsigned)blocks, 256, 0, st>>>(C, ldc, n, out);
+  HP_CHECK_LAUNCH("drift_kernel");
+  return HP_OK;
+}
+
+// ------------------------------------------------------------------ K6 signs
+// One CTA per mode: argmax |U[:,k]| (first index on ties), sign -> +1 if 0,
+// flip U[:,k] (and R[:,k] when given).  Optionally also writes the signed
+// sigma*sign scale the parent consumes.
+__global__ void signs_kernel(double* U, int64_t ldu, int64_t d, double* R, int64_t ldr, int64_t mr, double* sign_out) {
+  __shared__ double bv[256];
+  __shared__ int64_t bi[256];
+  __shared__ double sgn;
+  const int64_t k = blockIdx.x;
+  double* col = U + k * ldu;
+  double best = -1.0;
+  int64_t bidx = 0;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const double a = fabs(col[i]);
+    if (a > best) {
+      best = a;
+      bidx = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ov = bv[threadIdx.x + s];
+      const int64_t oi = bi[threadIdx.x + s];
+      if (ov > bv[threadIdx.x] || (ov == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = ov;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double v = col[bi[0]];
+    sgn = v < 0.0 ? -1.0 : 1.0;
+    if (sign_out) sign_out[k] = sgn;
+  }
+  __syncthreads();
+  if (sgn < 0.0) {
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) col[i] = -col[i];
+    if (R)
+      for (int64_t i = threadIdx.x; i < mr; i += blockDim.x) R[k * ldr + i] = -R[k * ldr + i];
+  }
+}
+
+int signs_run(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
+              cudaStream_t st) {
+  if (N == 0) return HP_OK;
+  signs_kernel<<<(unsigned)N, 256, 0, st>>>(U, ldu, d, R, ldr, mr, sign_out);
+  HP_CHECK_LAUNCH("signs_kernel");
+  return HP_OK;
+}
+
+// ------------------------------------------------------------------ Cholesky (CholQR)
+constexpr int CB = 64;
+
+// Factor the kb x kb diagonal block at A[k0,k0] (lower, in place), write
+// Dinv = (L_kk^{-1})^T col-major (ld CB) and flag a non-positive pivot.
+__global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_t k0, int kb, double* Dinv, int* info) {
+  extern __shared__ double pd_smem[];
+  double (*L)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(pd_smem);
+  double (*X)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(pd_smem + CB * (CB + 1));
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < CB * CB; e += 256) {
+    const int j = e / CB, i = e % CB;
+    L[i][j] = (i < kb && j < kb && i >= j) ? A[(k0 + j) * lda + k0 + i] : 0.0;
+    X[i][j] = 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    if (tid == 0) {
+      const double dj = L[j][j];
+      if (!(dj > 0.0)) {
+        bad = 1;
+        L[j][j] = 1.0;
+      } else {
+        L[j][j] = sqrt(dj);
+      }
+    }
+    __syncthreads();
+    const double piv = L[j][j];
+    for (int i = j + 1 + tid; i < kb; i += 256) L[i][j] /= piv;
+    __syncthreads();
+    const int rem = kb - j - 1;
+    for (int e = tid; e < rem * rem; e += 256) {
+      const int ii = j + 1 + e / rem, kk = j + 1 + e % rem;
+      if (kk <= ii) L[ii][kk] -= L[ii][j] * L[kk][j];
+    }
+    __syncthreads();
+  }
+  // X = L^{-1} by forward substitution, one column per thread
+  if (tid < kb) {
+    const int c = tid;
+    X[c][c] = 1.0 / L[c][c];
+    for (int i = c + 1; i < kb; ++i) {
+      double s = 0.0;
+      for (int q = c; q < i; ++q) s += L[i][q] * X[q][c];
+      X[i][c] = -s / L[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kb * kb; e += 256) {
+    const int j = e / kb, i = e % kb;
+    A[(k0 + j) * lda + k0 + i] = (i >= j) ? L[i][j] : 0.0;
+    // Dinv(k', n) = X(n, k') stored col-major with ld CB: Dinv[n*CB + k'] ... i.e. element (row i, col j) = X(j, i)
+    Dinv[j * CB + i] = X[j][i];
+  }
+  if (tid == 0 && bad) atomicOr(info, 1);
+}
+
+// Lower Cholesky of the n x n symmetric matrix A (lower part used, whole matrix
+// overwritten: lower = L, strict upper = 0).  Dinv receives the transposed
+// inverses of the diagonal blocks (nblk x CB x CB).
+int potrf_run(double* A, int64_t lda, int64_t n, double* Dinv, int* info, void* ws, size_t ws_bytes, cudaStream_t st) {
+  HP_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  const int pd_smem = 2 * CB * (CB + 1) * 8;
+  static bool configured = false;
+  if (!configured) {
+    HP_CHECK_CUDA(cudaFuncSetAttribute(potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem));
+    configured = true;
+  }
+  for (int64_t k0 = 0; k0 < n; k0 += CB) {
+    const int kb = (int)std::min<int64_t>(CB, n - k0);
+    double* Dk = Dinv + (k0 / CB) * CB * CB;
+    potrf_diag<<<1, 256, pd_smem, st>>>(A, lda, k0, kb, Dk, info);
+    HP_CHECK_LAUNCH("potrf_diag");
+    const int64_t rest = n - k0 - kb;
+    if (rest <= 0) continue;
+    double* P = A + k0 * lda + k0 + kb;  // panel rows k0+kb.., cols k0..k0+kb
+    // P <- P * L_kk^{-T}   (B(k', n) = Linv(n, k') = Dk[k' + n*CB] ... K-major columns of Dk^T)
+    VecSet a{P, lda, nullptr};
+    VecSet b{Dk, CB, nullptr};
+    // B(k', n) must equal (L^{-T})(k', n) = Linv(n, k') = X[n][k'] = Dk[k' * CB + n]
+    // as a K-major operand vector n is contiguous along k': Dk stored with element
+    // (i=k', j=n) at j*CB + i holds X[j][i]?  Dk[j*CB+i] = X[j][i] = Linv(j, i): vector n=j
+    // contiguous along k'=i gives Linv(n, k') -- exactly L^{-T}(k', n).
+    int rc = gemm_run(false, true, rest, kb, kb, a, b, (lda % 2 == 0), 1.0, 0.0, P, lda, nullptr, nullptr, nullptr,
+                      0, 0, nullptr, 0, st);
+    if (rc) return rc;
+    // trailing update A22 -= P P^T (symmetric)
+    double* A22 = A + (k0 + kb) * lda + k0 + kb;
+    VecSet pa{P, lda, nullptr};  // A operand: M-major, vector k' = column of P
+    VecSet pb{P, lda, nullptr};  // B operand N-major: B(k', n) = P(n, k'), vector k' contiguous along n
+    rc = gemm_run(false, false, rest, rest, kb, pa, pb, (lda % 2 == 0), -1.0, 1.0, A22, lda, nullptr, nullptr,
+                  nullptr, 1, 0, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  return HP_OK;
+}
+
+__global__ void copy_diag_inverse(const double* Dinv, int64_t n, double* Linv, int64_t ld) {
+  // Linv(i, j) for the diagonal blocks = X(i, j) = Dinv_blk[i_l*CB + j_l]... (Dinv[j*CB+i] = X[j][i])
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nblk = ceil_div(n, CB);
+  if (e >= nblk * CB * CB) return;
+  const int64_t blk = e / (CB * CB);
+  const int r = (int)(e % (CB * CB));
+  const int jl = r / CB, il = r % CB;  // element stored at Dinv[jl*CB+il] = X[jl][il]
+  const int64_t gi = blk * CB + jl, gj = blk * CB + il;  // X row jl, col il
+  if (gi < n && gj < n) Linv[gj * ld + gi] = Dinv[e];
+}
+
+// Linv = L^{-1} (lower), blocked by block rows:
+//   T = L[i, 0:i] Linv[0:i, 0:i];   Linv[i, 0:i] = -L_ii^{-1} T
+int trtri_run(const double* L, int64_t ldl, int64_t n, const double* Dinv, double* Linv, int64_t ldi, double* T,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  HP_CHECK_CUDA(cudaMemset2DAsync(Linv, ldi * 8, 0, n * 8, n, st));
+  const int64_t nblk = ceil_div(n, CB);
+  copy_diag_inverse<<<(unsigned)ceil_div(nblk * CB * CB, 256), 256, 0, st>>>(Dinv, n, Linv, ldi);
+  HP_CHECK_LAUNCH("copy_diag_inverse");
+  for (int64_t ib = 1; ib < nblk; ++ib) {
+    const int64_t r0 = ib * CB;
+    const int rb = (int)std::min<int64_t>(CB, n - r0);
+    // T (rb x r0) = L[r0:r0+rb, 0:r0] * Linv[0:r0, 0:r0]
+    VecSet a{L + r0, ldl, nullptr};      // M-major: vector k = column k of L, offset r0
+    VecSet b{Linv, ldi, nullptr};        // K-major: vector n = column n of Linv
+    int rc = gemm_run(false, true, rb, r0, r0, a, b, (ldl % 2 == 0) && (ldi % 2 == 0) && (r0 % 2 == 0), 1.0, 0.0, T,
+                      CB, nullptr, nullptr, nullptr, 0, 0, ws, ws_bytes, st);
+    if (rc) return rc;
+    // Linv[r0:r0+rb, 0:r0] = -Linv_ii * T ; A(m,k) = Linv_ii(m,k) = X[m][k] = Dinv[m*CB + k] -> K-major vector m
+    const double* Di = Dinv + ib * CB * CB;
+    VecSet a2{Di, CB, nullptr};
+    VecSet b2{T, CB, nullptr};           // K-major: vector n = column n of T
+    rc = gemm_run(true, true, rb, r0, rb, a2, b2, true, -1.0, 0.0, Linv + r0, ldi, nullptr, nullptr, nullptr, 0, 0,
+                  ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  return HP_OK;
+}
+
+// ------------------------------------------------------------------ layout helpers
+__global__ void transpose_rm_to_cm(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd) {
+  // src row-major rows x cols; dst col-major with leading dimension ldd
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += 8) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (r < rows && c < cols) ? src[r * cols + c] : 0.0;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += 8) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][dy];
+  }
+}
+
+int transpose_run(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return HP_OK;
+  dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+  transpose_rm_to_cm<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd);
+  HP_CHECK_LAUNCH("transpose_rm_to_cm");
+  return HP_OK;
+}
+
+// dst[:, j] = src[:, j] * (rs ? rs[i] : 1) / (rd ? rd[i] : 1) * (cs ? cs[j] : 1)
+__global__ void scale_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* rs,
+                             const double* rd, const double* cs, double* dst, int64_t ldd) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t j = e / rows, i = e % rows;
+  double v = src[j * lds + i];
+  if (rs) v *= rs[i];
+  if (rd) v /= rd[i];
+  if (cs) v *= cs[j];
+  dst[j * ldd + i] = v;
+}
+
+int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* rs, const double* rd,
+              const double* cs, double* dst, int64_t ldd, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return HP_OK;
+  scale_kernel<<<(unsigned)ceil_div(rows * cols, 256), 256, 0, st>>>(src, lds, rows, cols, rs, rd, cs, dst, ldd);
+  HP_CHECK_LAUNCH("scale_kernel");
+  return HP_OK;
+}
+
+__global__ void finite_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t j = e / rows, i = e % rows;
+  const double v = src[j * lds + i];
+  if (!isfinite(v)) atomicOr(bad, 1);
+}
+
+int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st) {
+  HP_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  if (rows == 0 || cols == 0) return HP_OK;
+  finite_kernel<<<(unsigned)ceil_div(rows * cols, 256), 256, 0, st>>>(src, lds, rows, cols, bad);
+  HP_CHECK_LAUNCH("finite_kernel");
+  return HP_OK;
+}
+
+// ------------------------------------------------------------------ sum of squares
+// Deterministic two-pass reduction: fixed per-block partials, then one block
+// sums them in index order (residual energy of actual_mean_error,
+// hierarchy.py:249-253).
+constexpr int SQ_BLOCKS = 1024;
+
+__global__ void sumsq_partial(const double* A, int64_t lda, int64_t rows, int64_t cols, double* partial) {
+  __shared__ double red[256];
+  const int64_t total = rows * cols;
+  double s = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)SQ_BLOCKS * 256) {
+    const int64_t j = e / rows, i = e % rows;
+    const double v = A[j * lda + i];
+    s += v * v;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void sumsq_final(const double* partial, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < SQ_BLOCKS; i += 256) s += partial[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, double* partial,
+              cudaStream_t st) {
+  sumsq_partial<<<SQ_BLOCKS, 256, 0, st>>>(A, lda, rows, cols, partial);
+  HP_CHECK_LAUNCH("sumsq_partial");
+  sumsq_final<<<1, 256, 0, st>>>(partial, out);
+  HP_CHECK_LAUNCH("sumsq_final");
+  return HP_OK;
+}
+
+}  // namespace hp

@@ -1,0 +1,192 @@
+"""Kernel-level parity of libhapod_b200.so against the CPU oracle / numpy, called
+through the C-ABI (ctypes).  Needs a B200."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1607_05210_b200 import _device as D  # noqa: E402
+from paper_1607_05210_b200 import _native as N  # noqa: E402
+
+lib = N.load()
+
+
+def st():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ws(nbytes):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
+
+
+@pytest.mark.parametrize("d,m", [(1, 1), (7, 3), (100, 17), (1000, 128), (4099, 129), (20000, 512), (3, 300)])
+def test_gram_matches_numpy(d, m):
+    rng = np.random.default_rng(d * 7 + m)
+    a = rng.standard_normal((d, m))
+    A = D.upload(a)
+    G = D.DevMat.empty(m, m)
+    w = ws(lib.hp_gram_workspace_bytes(d, m))
+    N.check(lib.hp_gram(A.vecset(), d, m, None, G.ptr, G.ld, w.data_ptr(), w.numel(), st()), "gram")
+    g = G.to_numpy()
+    ref = a.T @ a
+    assert np.array_equal(g, g.T)  # exactly symmetric
+    assert np.max(np.abs(g - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(d)
+
+
+@pytest.mark.parametrize("odd", [False, True])
+def test_gram_colscale_and_table(odd):
+    rng = np.random.default_rng(5)
+    d = 333 if odd else 334
+    parts = [rng.standard_normal((d, c)) for c in (5, 0, 40, 13)]
+    scales = [rng.uniform(0.5, 2.0, p.shape[1]) for p in parts]
+    devparts = [D.Part(D.upload(p), torch.from_numpy(s).cuda()) for p, s in zip(parts, scales)]
+    G, m, keep = D.gram_full(devparts, d)
+    joined = np.hstack([p * s for p, s in zip(parts, scales)])
+    ref = joined.T @ joined
+    assert np.allclose(G.to_numpy(), ref, rtol=1e-13, atol=1e-12)
+
+
+@pytest.mark.parametrize("M,N_,K", [(1, 1, 1), (300, 70, 33), (20000, 257, 512), (129, 130, 1000)])
+def test_gemm_nn_with_divide(M, N_, K):
+    rng = np.random.default_rng(M + N_ + K)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N_))
+    dv = rng.uniform(0.5, 2.0, N_)
+    A, B = D.upload(a), D.upload(b)
+    C = D.DevMat.empty(M, N_)
+    dvd = torch.from_numpy(dv).cuda()
+    w = ws(lib.hp_gemm_workspace_bytes(M, N_, K, 0, 0))
+    N.check(lib.hp_gemm(0, 1, M, N_, K, A.vecset(), B.vecset(), 1.0, 0.0, C.ptr, C.ld, None, None, dvd.data_ptr(),
+                        0, 0, w.data_ptr(), w.numel(), st()), "gemm")
+    ref = (a @ b) / dv[None, :]
+    assert np.allclose(C.to_numpy(), ref, rtol=1e-12, atol=1e-11)
+
+
+def test_gemm_nt_sym_and_upper():
+    rng = np.random.default_rng(3)
+    M, K = 200, 64
+    p = rng.standard_normal((M, K))
+    c0 = rng.standard_normal((M, M))
+    c0 = c0 + c0.T
+    P, C = D.upload(p), D.upload(c0)
+    w = ws(lib.hp_gemm_workspace_bytes(M, M, K, 1, 0))
+    N.check(lib.hp_gemm(0, 0, M, M, K, P.vecset(), P.vecset(), -1.0, 1.0, C.ptr, C.ld, None, None, None, 1, 0,
+                        w.data_ptr(), w.numel(), st()), "syrk")
+    assert np.allclose(C.to_numpy(), c0 - p @ p.T, rtol=1e-12, atol=1e-11)
+    # upper-triangular B, N-major
+    x = rng.standard_normal((500, 150))
+    l = np.tril(rng.standard_normal((150, 150)))
+    X, L = D.upload(x), D.upload(l)
+    Y = D.DevMat.empty(500, 150)
+    N.check(lib.hp_gemm(0, 0, 500, 150, 150, X.vecset(), L.vecset(), 1.0, 0.0, Y.ptr, Y.ld, None, None, None, 0, 1,
+                        None, 0, st()), "trmm")
+    assert np.allclose(Y.to_numpy(), x @ l.T, rtol=1e-12, atol=1e-11)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 64, 65, 200, 512, 1000])
+def test_syev_matches_eigh(n):
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.sort(rng.uniform(-1, 4, n))[::-1]
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    G = D.upload(g)
+    lam_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    V = D.DevMat.empty(n, n)
+    w = ws(lib.hp_syev_workspace_bytes(n))
+    sweeps = ctypes.c_int(0)
+    N.check(lib.hp_syev(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 60,
+                        ctypes.byref(sweeps), w.data_ptr(), w.numel(), st()), "syev")
+    ev = lam_d.cpu().numpy()
+    ref = np.linalg.eigvalsh(g)[::-1]
+    print("syev n", n, "sweeps", sweeps.value, "err", np.max(np.abs(ev - ref)))
+    assert np.all(np.diff(ev) <= 0)
+    assert np.allclose(ev, ref, rtol=0, atol=1e-13 * max(1, np.abs(ref).max()) * np.sqrt(n))
+    v = V.to_numpy()
+    assert np.max(np.abs(v.T @ v - np.eye(n))) < 1e-12 * np.sqrt(n)
+    assert np.max(np.abs(g @ v - v * ev[None, :])) < 1e-12 * np.sqrt(n) * max(1, np.abs(ref).max())
+
+
+def test_syev_graded_psd_gram():
+    # a method-of-snapshots Gramian with a 1e-16 spread, as in SURVEY 0.2
+    rng = np.random.default_rng(1)
+    d, m = 3000, 300
+    q1, _ = np.linalg.qr(rng.standard_normal((d, m)))
+    q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    sig = 10.0 ** (-8 * np.arange(m) / (m - 1))
+    s = (q1 * sig) @ q2.T
+    g = s.T @ s
+    g = 0.5 * (g + g.T)
+    G = D.upload(g)
+    lam_d = torch.empty(m, dtype=torch.float64, device="cuda")
+    V = D.DevMat.empty(m, m)
+    w = ws(lib.hp_syev_workspace_bytes(m))
+    sweeps = ctypes.c_int(0)
+    N.check(lib.hp_syev(G.ptr, G.ld, m, lam_d.data_ptr(), V.ptr, V.ld, m, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 60,
+                        ctypes.byref(sweeps), w.data_ptr(), w.numel(), st()), "syev")
+    ev = lam_d.cpu().numpy()
+    import scipy.linalg
+    ref = scipy.linalg.eigh(g, eigvals_only=True)[::-1]
+    keep = ref >= 4 * 2.0 ** -52 * ref[0] * m
+    err = np.abs(ev[keep] - ref[keep]) / ref[0]
+    print("graded: sweeps", sweeps.value, "max abs err / lam_max", err.max())
+    assert err.max() < 1e-14
+    v = V.to_numpy()
+    print("graded: V orthogonality", np.max(np.abs(v.T @ v - np.eye(m))))
+    assert np.max(np.abs(v.T @ v - np.eye(m))) < 1e-13
+
+
+def test_truncate_kernel_matches_rule():
+    from oracle.hapod_oracle import truncation_rank
+    rng = np.random.default_rng(9)
+    for trial in range(20):
+        n = int(rng.integers(1, 3000))
+        lam = np.sort(rng.exponential(1.0, n) ** 4)[::-1]
+        eps = float(rng.uniform(0, 1) * np.sqrt(lam.sum()))
+        cutoff = 4 * 2.0 ** -52
+        ld = torch.from_numpy(lam.copy()).cuda()
+        sig = torch.empty(n, dtype=torch.float64, device="cuda")
+        info = torch.empty(4, dtype=torch.float64, device="cuda")
+        N.check(lib.hp_truncate(ld.data_ptr(), n, eps, cutoff, n, sig.data_ptr(), info.data_ptr(), st()), "trunc")
+        lam_max, nkeep, N_, tail = info.cpu().tolist()
+        keep = lam >= cutoff * lam[0] * n
+        s = np.sqrt(lam[keep])
+        assert int(nkeep) == keep.sum()
+        assert int(N_) == truncation_rank(s, eps)
+        assert tail == pytest.approx(float(np.sum(lam[keep][int(N_):])), rel=1e-12, abs=1e-300)
+
+
+def test_signs_and_reortho():
+    rng = np.random.default_rng(2)
+    d, n = 5000, 200
+    # badly conditioned but full-rank columns -> drift > 1e-8
+    q, _ = np.linalg.qr(rng.standard_normal((d, n)))
+    u = q @ (np.eye(n) + 1e-5 * rng.standard_normal((n, n)))
+    U = D.upload(u)
+    C = D.DevMat.empty(n, n)
+    drift = torch.zeros(1, dtype=torch.float64, device="cuda")
+    w = ws(lib.hp_drift_workspace_bytes(d, n))
+    N.check(lib.hp_drift(U.ptr, U.ld, d, n, C.ptr, C.ld, drift.data_ptr(), w.data_ptr(), w.numel(), st()), "drift")
+    ref_drift = np.max(np.abs(u.T @ u - np.eye(n)))
+    assert float(drift.item()) == pytest.approx(ref_drift, rel=1e-6)
+    w = ws(lib.hp_reortho_workspace_bytes(d, n))
+    passes = ctypes.c_int(0)
+    N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n, C.ptr, C.ld, ctypes.byref(passes), w.data_ptr(), w.numel(),
+                                    st()), "reortho")
+    qq = U.to_numpy()
+    assert np.max(np.abs(qq.T @ qq - np.eye(n))) < 1e-13
+    # same Q as Gram-Schmidt (positive diagonal R)
+    qr_q, r = np.linalg.qr(u)
+    qr_q = qr_q * np.sign(np.diag(r))[None, :]
+    assert np.max(np.abs(qq - qr_q)) < 1e-9
+    N.check(lib.hp_signs(U.ptr, U.ld, d, n, None, 0, 0, None, st()), "signs")
+    s = U.to_numpy()
+    pick = np.argmax(np.abs(s), axis=0)
+    assert np.all(s[pick, np.arange(n)] > 0)
