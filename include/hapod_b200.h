@@ -47,6 +47,8 @@ typedef struct hp_vecset {
 } hp_vecset;
 
 int hp_abi_version(void);
+/* Number of kernels this library has launched in the process (monotonic). */
+long long hp_launch_count(void);
 const char* hp_last_error(void);
 int hp_device_sm_count(int device);
 
@@ -82,10 +84,13 @@ int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F
 /* K2 -- all eigenpairs of the symmetric n x n G, eigenvalues descending,
  * first nvec eigenvectors in V.  Replaces scipy.linalg.eigh + reversal
  * (pod.py:329-331, 386-388).  Parallel two-sided block Jacobi; synchronises
- * the stream once per sweep.  Returns HP_ELINALG if max_sweeps is reached. */
+ * the stream once per sweep.  Returns HP_ELINALG if max_sweeps is reached.
+ * sweeps / flops (nullable, host) receive the sweep count and the algorithmic
+ * flops of its DMMA products. */
 size_t hp_syev_workspace_bytes(int64_t n);
 int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, void* ws, size_t ws_bytes, void* stream);
+            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, double* flops, void* ws, size_t ws_bytes,
+            void* stream);
 
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
  * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank

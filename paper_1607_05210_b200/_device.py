@@ -34,6 +34,52 @@ JACOBI_TOL_ABS = 16 * 2.0 ** -52  # absolute off-diagonal trigger, x max|g_ii| (
 JACOBI_MAX_SWEEPS = 60
 
 
+class Profiler:
+    """Optional CUDA-event timing of the node phases on the launching stream
+    (used by bench.py for the live roofline; off by default)."""
+
+    enabled = False
+    records: list = []
+
+    @classmethod
+    def reset(cls, enabled=True):
+        cls.enabled = enabled
+        cls.records = []
+
+    @classmethod
+    def summary(cls):
+        """{phase: (launches, total_ms, total_flops)} -- synchronises the device."""
+        out: dict = {}
+        if cls.records:
+            torch.cuda.synchronize()
+        for name, e0, e1, flops in cls.records:
+            n, ms, f = out.get(name, (0, 0.0, 0.0))
+            out[name] = (n + 1, ms + e0.elapsed_time(e1), f + flops)
+        return out
+
+
+class _phase:
+    __slots__ = ("name", "flops", "e0")
+
+    def __init__(self, name, flops=0.0):
+        self.name = name
+        self.flops = float(flops)
+        self.e0 = None
+
+    def __enter__(self):
+        if Profiler.enabled:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        if self.e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            Profiler.records.append((self.name, self.e0, e1, self.flops))
+        return False
+
+
 def require_cuda():
     if torch is None or not torch.cuda.is_available():
         raise RuntimeError("the HAPOD B200 path needs a CUDA device (there is no CPU fallback)")
@@ -222,7 +268,8 @@ def gram_full(parts: list[Part], d: int):
     G = DevMat.empty(m, m)
     if m:
         ws = _ws(lib.hp_gram_workspace_bytes(d, m))
-        N.check(lib.hp_gram(vs, d, m, _ptr(scale), G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "gram")
+        with _phase("gram", float(d) * m * (m + 1)):
+            N.check(lib.hp_gram(vs, d, m, _ptr(scale), G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "gram")
     return G, m, keep
 
 
@@ -235,8 +282,9 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     total = n_old + m
     G = DevMat.empty(total, total)
     ws = _ws(lib.hp_block_gram_workspace_bytes(d, n_old, m))
-    N.check(lib.hp_block_gram(prior_U.vecset(), prior_sig_dev.data_ptr(), n_old, vs_f, _ptr(scale_f), m, d,
-                              G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "block gram")
+    with _phase("gram", 2.0 * d * n_old * m + float(d) * m * (m + 1)):
+        N.check(lib.hp_block_gram(prior_U.vecset(), prior_sig_dev.data_ptr(), n_old, vs_f, _ptr(scale_f), m, d,
+                                  G.ptr, G.ld, ws.data_ptr(), ws.numel(), _stream()), "block gram")
     return G, total, keep
 
 
@@ -250,13 +298,19 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     V = DevMat.empty(m, m)
     ws = _ws(lib.hp_syev_workspace_bytes(m))
     sweeps = ctypes.c_int(0)
-    N.check(lib.hp_syev(G.ptr, G.ld, m, lam.data_ptr(), V.ptr, V.ld, m, JACOBI_TOL_REL, JACOBI_TOL_ABS,
-                        JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ws.data_ptr(), ws.numel(), st), "eigensolve")
+    eflops = ctypes.c_double(0.0)
+    ph = _phase("eigensolve")
+    with ph:
+        N.check(lib.hp_syev(G.ptr, G.ld, m, lam.data_ptr(), V.ptr, V.ld, m, JACOBI_TOL_REL, JACOBI_TOL_ABS,
+                            JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
+                            ws.numel(), st), "eigensolve")
+        ph.flops = eflops.value
     del ws
     sig = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
     info = torch.empty(4, dtype=torch.float64, device="cuda")
-    N.check(lib.hp_truncate(lam.data_ptr(), m, float(eps), float(cutoff), m, sig.data_ptr(), info.data_ptr(), st),
-            "truncate")
+    with _phase("truncate"):
+        N.check(lib.hp_truncate(lam.data_ptr(), m, float(eps), float(cutoff), m, sig.data_ptr(), info.data_ptr(),
+                                st), "truncate")
     lam_max, nkeep, n_modes, tail = info.cpu().tolist()
     nkeep, n_modes = int(nkeep), int(n_modes)
     if not (lam_max > 0.0):
@@ -279,23 +333,27 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         Vs = Vn
     U = DevMat.empty(d, n_modes)
     ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
-    N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld, ws.data_ptr(),
-                            ws.numel(), st), "assemble")
+    with _phase("assemble", 2.0 * d * m * n_modes):
+        N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld,
+                                ws.data_ptr(), ws.numel(), st), "assemble")
     del ws, Vs
     # drift = max |U^T W U - I| (U is in Euclidean coordinates when weighted)
     C = DevMat.empty(n_modes, n_modes)
     drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
     ws = _ws(lib.hp_drift_workspace_bytes(d, n_modes))
-    N.check(lib.hp_drift(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
-            "drift")
+    with _phase("drift", float(d) * n_modes * (n_modes + 1)):
+        N.check(lib.hp_drift(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(),
+                             st), "drift")
     del ws
     drift = float(drift_dev.item())
     reorthed = False
     if drift > DRIFT_TOL:
         ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
         passes = ctypes.c_int(0)
-        N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, ctypes.byref(passes),
-                                        ws.data_ptr(), ws.numel(), st), "re-orthonormalisation")
+        # CholQR2: pass 1 reuses the drift Gram (U L^-T: d N^2), pass 2 = SYRK + U L^-T
+        with _phase("reortho", float(d) * n_modes * n_modes * 2 + float(d) * n_modes * (n_modes + 1)):
+            N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, ctypes.byref(passes),
+                                            ws.data_ptr(), ws.numel(), st), "re-orthonormalisation")
         del ws
         reorthed = True
     del C
@@ -304,8 +362,9 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     R = None
     if want_right:
         R = V.view_cols(0, n_modes).clone()
-    N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None, R.ld if R is not None else 0,
-                         m if R is not None else 0, None, st), "signs")
+    with _phase("signs"):
+        N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None,
+                             R.ld if R is not None else 0, m if R is not None else 0, None, st), "signs")
     sig_host = sig_dev.cpu().numpy()
     return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps.value, m)
 

@@ -31,6 +31,7 @@ class VecSet(ctypes.Structure):
 
 _SIGNATURES = {
     "hp_abi_version": (c_int, []),
+    "hp_launch_count": (ctypes.c_longlong, []),
     "hp_last_error": (ctypes.c_char_p, []),
     "hp_device_sm_count": (c_int, [c_int]),
     "hp_gemm_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_int, c_int]),
@@ -42,7 +43,7 @@ _SIGNATURES = {
     "hp_block_gram": (c_int, [VecSet, c_vp, c_i64, VecSet, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_size, c_vp]),
     "hp_syev_workspace_bytes": (c_size, [c_i64]),
     "hp_syev": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_int,
-                        ctypes.POINTER(c_int), c_vp, c_size, c_vp]),
+                        ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), c_vp, c_size, c_vp]),
     "hp_truncate": (c_int, [c_vp, c_i64, c_dbl, c_dbl, c_i64, c_vp, c_vp, c_vp]),
     "hp_assemble_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "hp_assemble": (c_int, [VecSet, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_size, c_vp]),

@@ -2,6 +2,7 @@
 // Plain pointers and sizes only; every entry returns an hp status code and
 // leaves a thread-local message for hp_last_error().
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -11,6 +12,8 @@
 namespace hp {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
@@ -26,8 +29,8 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
 size_t syev_workspace_bytes(int64_t n);
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, void* ws, size_t ws_bytes,
-             cudaStream_t st);
+             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, double* flops_out, void* ws,
+             size_t ws_bytes, cudaStream_t st);
 int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
                  cudaStream_t st);
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
@@ -147,6 +150,7 @@ using namespace hp;
 extern "C" {
 
 int hp_abi_version(void) { return HP_ABI_VERSION; }
+long long hp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* hp_last_error(void) { return hp::last_error(); }
 
 int hp_device_sm_count(int device) {
@@ -204,8 +208,9 @@ int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F
 size_t hp_syev_workspace_bytes(int64_t n) { return syev_workspace_bytes(n); }
 
 int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, void* ws, size_t ws_bytes, void* stream) {
-  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, max_sweeps, sweeps, ws, ws_bytes,
+            double tol_rel, double tol_abs, int max_sweeps, int* sweeps, double* flops, void* ws, size_t ws_bytes,
+            void* stream) {
+  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, max_sweeps, sweeps, flops, ws, ws_bytes,
                   (cudaStream_t)stream);
 }
 

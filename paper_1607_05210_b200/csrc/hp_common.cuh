@@ -32,8 +32,12 @@ const char* last_error();
     }                                                                                \
   } while (0)
 
+// number of kernels this library launched (bench.py's gpu_launches)
+void count_launches(long long n);
+
 #define HP_CHECK_LAUNCH(what)                                                        \
   do {                                                                               \
+    ::hp::count_launches(1);                                                         \
     cudaError_t _e = cudaGetLastError();                                             \
     if (_e != cudaSuccess) {                                                         \
       ::hp::set_error(std::string("launch ") + (what) + ": " + cudaGetErrorString(_e)); \

@@ -32,6 +32,8 @@
 // by index at the end.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "hp_common.cuh"
@@ -46,7 +48,7 @@ namespace jac {
 constexpr int BW = 32;        // block width
 constexpr int PS = 2 * BW;    // local problem size
 constexpr int LS = PS + 1;    // local smem stride
-constexpr int LT = 256;       // local solver threads
+constexpr int LT = 512;       // local solver threads
 constexpr int TS = PS + 4;    // apply-kernel smem stride (= 4 mod 16: conflict-free DMMA fragments)
 constexpr int AT = 256;       // apply threads
 
@@ -60,6 +62,7 @@ struct Params {
   int* flags;         // nb/2
   int* counter;       // pairs that needed work in this sweep
   double* maxoff;     // max |g_ij| / max|g_ii| seen in this sweep (atomic max on the bit pattern)
+  unsigned long long* mm_count;  // 64x64x64 DMMA products performed by jac_apply (flop accounting)
   const double* scal; // scal[0] = max |g_ii| of the input
   double tol_rel, tol_abs;
   int max_local_sweeps;
@@ -106,6 +109,8 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
   block_pair(p, k, bp, bq);
   const int tid = threadIdx.x;
   const double tr = p.tol_rel, ta = p.tol_abs * p.scal[0];
+  // local floor: entries below u*max|g_ii| are rounding noise -- do not chase them
+  const double tloc = 2.220446049250313e-16 * p.scal[0];
 
   for (int e = tid; e < PS * PS; e += LT) {
     const int j = e / PS, i = e % PS;
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
         int a, b;
         circle_pair(PS, step, tid, a, b);
         const double aii = A[a * LS + a], ajj = A[b * LS + b], aij = A[a * LS + b];
-        int r = needs_rotation(aij, aii, ajj, tr, 1e-300 * p.scal[0]);
+        int r = needs_rotation(aij, aii, ajj, tr, tloc);
         double c = 1.0, s = 0.0, t = 0.0;
         if (r) {
           const double theta = (ajj - aii) / (2.0 * aij);
@@ -222,6 +227,19 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     }
     if (!any_rot) break;
   }
+  // sorted Jacobi: order the local eigenvalues descending so large eigenvalues
+  // migrate to the low blocks (the rank-of-diagonal permutation of W's columns)
+  __shared__ int sperm[PS];
+  if (tid < PS) {
+    const double di = A[tid * LS + tid];
+    int r = 0;
+    for (int j = 0; j < PS; ++j) {
+      const double dj = A[j * LS + j];
+      r += (dj > di) || (dj == di && j < tid);
+    }
+    sperm[r] = tid;
+  }
+  __syncthreads();
   // one Bjorck step: E = I - W^T W ; W <- W + W E / 2   (result staged in A's buffer)
   double* E = Wl + PS * LS;
   for (int e = tid; e < PS * PS; e += LT) {
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
   __syncthreads();
   for (int e = tid; e < PS * PS; e += LT) {
     const int j = e / PS, i = e % PS;
-    p.W[(int64_t)k * PS * PS + j * PS + i] = A[i * LS + j];
+    p.W[(int64_t)k * PS * PS + j * PS + i] = A[i * LS + sperm[j]];
   }
   if (tid == 0) {
     p.flags[k] = 1;
@@ -322,6 +340,7 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
     }
     if (fQ) load_w(WQ, p.W + (int64_t)Q * PS * PS);
     if (fP) load_w(WP, p.W + (int64_t)P * PS * PS);
+    if (threadIdx.x == 0) atomicAdd(p.mm_count, (unsigned long long)(fP + fQ));
     __syncthreads();
     if (fQ) {
       mm64<false>(X, WQ, acc);  // X W_Q
@@ -366,6 +385,7 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
     X[j * TS + i] = p.V[local_index(qp, qq, j) * p.np + rc * PS + i];
   }
   load_w(WQ, p.W + (int64_t)Q * PS * PS);
+  if (threadIdx.x == 0) atomicAdd(p.mm_count, 1ull);
   __syncthreads();
   mm64<false>(X, WQ, acc);
   __syncthreads();
@@ -401,10 +421,13 @@ __global__ void max_abs_diag(const double* Gp, int64_t np, int64_t n, double* ou
 // Rayleigh quotients against the ORIGINAL Gramian: rq_i = v_i^T (G0 v_i), one
 // warp per column, fixed summation order (deterministic).  Removes the
 // eigenvalue drift that the accumulated local rotations leave in diag(G).
-__global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t ldy, int64_t n, double* out) {
+// Columns whose real part (rows < n) vanishes are padding eigenvectors (exact
+// unit vectors of the zero padding, never mixed with real coordinates): -inf.
+__global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t ldy, int64_t n, int64_t ncols,
+                        double* out) {
   const int64_t col = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (col >= n) return;
+  if (col >= ncols) return;
   double s = 0.0, nn = 0.0;
   for (int64_t k = lane; k < n; k += 32) {
     const double v = V[col * ldv + k];
@@ -416,11 +439,11 @@ __global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t l
     s += __shfl_xor_sync(0xffffffffu, s, o);
     nn += __shfl_xor_sync(0xffffffffu, nn, o);
   }
-  if (lane == 0) out[col] = s / nn;
+  if (lane == 0) out[col] = nn > 0.5 ? s / nn : -INFINITY;
 }
 
 // rank of each value in descending order, ties broken by index
-__global__ void sort_rank(const double* dvals, int64_t n, double* lam, int* perm) {
+__global__ void sort_rank(const double* dvals, int64_t n, int64_t keep, double* lam, int* perm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double di = dvals[i];
@@ -429,8 +452,10 @@ __global__ void sort_rank(const double* dvals, int64_t n, double* lam, int* perm
     const double dj = dvals[j];
     r += (dj > di) || (dj == di && j < i);
   }
-  lam[r] = di;
-  perm[r] = (int)i;
+  if (r < keep) {
+    lam[r] = di;
+    perm[r] = (int)i;
+  }
 }
 
 __global__ void gather_vectors(const double* Vp, int64_t np, int64_t n, const int* perm, int64_t nvec, double* V,
@@ -465,15 +490,15 @@ Layout layout(int64_t n) {
   L.off_flags = o;
   o = al(o + (size_t)(nb / 2) * 4);
   L.off_counter = o;
-  o = al(o + 32);
+  o = al(o + 64);
   L.off_scal = o;
   o = al(o + 16);
   L.off_perm = o;
-  o = al(o + (size_t)std::max<int64_t>(n, 1) * 4);
+  o = al(o + (size_t)L.np * 4);
   L.off_rq = o;
-  o = al(o + (size_t)std::max<int64_t>(n, 1) * 8);
+  o = al(o + (size_t)L.np * 8);
   L.off_gemm = o;
-  o = al(o + gemm_workspace_bytes(n, n, n, 0, 0));
+  o = al(o + gemm_workspace_bytes(n, L.np, n, 0, 0));
   L.total = o;
   return L;
 }
@@ -483,8 +508,8 @@ Layout layout(int64_t n) {
 size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
 
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, void* ws, size_t ws_bytes,
-             cudaStream_t st) {
+             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, double* flops_out, void* ws,
+             size_t ws_bytes, cudaStream_t st) {
   using namespace jac;
   HP_REQUIRE(n >= 0, "syev: negative order");
   if (sweeps_out) *sweeps_out = 0;
@@ -501,6 +526,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.flags = reinterpret_cast<int*>(base + L.off_flags);
   p.counter = reinterpret_cast<int*>(base + L.off_counter);
   p.maxoff = reinterpret_cast<double*>(base + L.off_counter + 16);
+  p.mm_count = reinterpret_cast<unsigned long long*>(base + L.off_counter + 24);
   double* scal = reinterpret_cast<double*>(base + L.off_scal);
   p.scal = scal;
   int* perm = reinterpret_cast<int*>(base + L.off_perm);
@@ -508,7 +534,8 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.nb = L.nb;
   p.tol_rel = tol_rel;
   p.tol_abs = tol_abs;
-  p.max_local_sweeps = 40;
+  static const int local_sweeps = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 1;
+  p.max_local_sweeps = local_sweeps;
 
   static bool configured = false;
   const int local_smem = 3 * PS * LS * 8;
@@ -528,19 +555,23 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   const int64_t napply = (int64_t)npairs * (npairs + 1) / 2 + (L.np / PS) * npairs;
   char* host_buf = nullptr;
   HP_CHECK_CUDA(cudaMallocHost(&host_buf, 32));
+  HP_CHECK_CUDA(cudaMemsetAsync(p.mm_count, 0, 8, st));
   int status = HP_ELINALG;
   int sweep = 0;
   double prev_off = INFINITY;
+  unsigned long long mm_total = 0;
   const double floor_ratio = 512.0 * 2.220446049250313e-16;
+  static const bool trace = getenv("HP_JACOBI_TRACE") != nullptr;
   for (; sweep < max_sweeps; ++sweep) {
-    cudaError_t e = cudaMemsetAsync(p.counter, 0, 32, st);
+    cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
     if (e != cudaSuccess) break;
     for (int r = 0; r < L.nb - 1; ++r) {
       p.round = r;
       jac_local<<<npairs, LT, local_smem, st>>>(p);
       jac_apply<<<(unsigned)napply, AT, apply_smem, st>>>(p);
+      count_launches(2);
     }
-    e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       cudaFreeHost(host_buf);
@@ -549,6 +580,9 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     }
     const int worked = *reinterpret_cast<int*>(host_buf);
     const double off = *reinterpret_cast<double*>(host_buf + 16);
+    mm_total = *reinterpret_cast<unsigned long long*>(host_buf + 24);
+    if (trace) fprintf(stderr, "[hp_syev n=%lld] sweep %d: pairs worked %d / %d, max off/diag %.3e\n", (long long)n,
+                       sweep, worked, npairs * (L.nb - 1), off);
     if (worked == 0 || (off < floor_ratio && off > 0.5 * prev_off)) {
       status = HP_OK;
       break;
@@ -557,6 +591,8 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   }
   cudaFreeHost(host_buf);
   if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
+  // algorithmic flops of the DMMA rotation products (+ the Rayleigh-quotient GEMM below)
+  if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + 2.0 * (double)n * n * (double)L.np;
   if (status != HP_OK) {
     set_error("syev: Jacobi iteration did not converge");
     return HP_ELINALG;
@@ -566,13 +602,14 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     VecSet a{G, ldg, nullptr};
     VecSet b{p.V, L.np, nullptr};
     const bool al16 = (ldg % 2 == 0) && ((uintptr_t)G % 16 == 0);
-    int rc = gemm_run(false, true, n, n, n, a, b, al16, 1.0, 0.0, p.G, L.np, nullptr, nullptr, nullptr, 0, 0,
+    int rc = gemm_run(false, true, n, L.np, n, a, b, al16, 1.0, 0.0, p.G, L.np, nullptr, nullptr, nullptr, 0, 0,
                       base + L.off_gemm, L.total - L.off_gemm, st);
     if (rc) return rc;
     double* rq = reinterpret_cast<double*>(base + L.off_rq);
-    rq_diag<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, rq);
+    rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, L.np, rq);
     HP_CHECK_LAUNCH("rq_diag");
-    sort_rank<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(rq, n, lam_desc, perm);
+    // rank all n_p columns (padding last), keep the first n
+    sort_rank<<<(unsigned)ceil_div(L.np, 256), 256, 0, st>>>(rq, L.np, n, lam_desc, perm);
     HP_CHECK_LAUNCH("sort_rank");
   }
   if (nvec > 0) {

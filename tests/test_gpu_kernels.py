@@ -103,7 +103,7 @@ def test_syev_matches_eigh(n):
     w = ws(lib.hp_syev_workspace_bytes(n))
     sweeps = ctypes.c_int(0)
     N.check(lib.hp_syev(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 60,
-                        ctypes.byref(sweeps), w.data_ptr(), w.numel(), st()), "syev")
+                        ctypes.byref(sweeps), None, w.data_ptr(), w.numel(), st()), "syev")
     ev = lam_d.cpu().numpy()
     ref = np.linalg.eigvalsh(g)[::-1]
     print("syev n", n, "sweeps", sweeps.value, "err", np.max(np.abs(ev - ref)))
@@ -130,7 +130,7 @@ def test_syev_graded_psd_gram():
     w = ws(lib.hp_syev_workspace_bytes(m))
     sweeps = ctypes.c_int(0)
     N.check(lib.hp_syev(G.ptr, G.ld, m, lam_d.data_ptr(), V.ptr, V.ld, m, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 60,
-                        ctypes.byref(sweeps), w.data_ptr(), w.numel(), st()), "syev")
+                        ctypes.byref(sweeps), None, w.data_ptr(), w.numel(), st()), "syev")
     ev = lam_d.cpu().numpy()
     import scipy.linalg
     ref = scipy.linalg.eigh(g, eigvals_only=True)[::-1]
