@@ -81,6 +81,17 @@ size_t hp_block_gram_workspace_bytes(int64_t d, int64_t n_old, int64_t m);
 int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F, const double* fscale, int64_t m,
                   int64_t d, double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream);
 
+/* K2a -- eigensolver preconditioner: pivoted Cholesky G = L L^T + E with
+ * complete diagonal pivoting, L (m x r) with rows in the ORIGINAL order, until
+ * the largest remaining pivot <= tol_rel * max|G_ii| (E = rounding noise).
+ * The eigenvalues of G are those of H = L^T L; its eigenvectors
+ * V = L W Lambda^{-1/2} (W = eigenvectors of H).  piv (device, m ints)
+ * receives the pivot order; rank (host) receives r.  Synchronises once per
+ * 64-column panel. */
+size_t hp_pstrf_workspace_bytes(int64_t m);
+int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
+             int64_t* rank, void* ws, size_t ws_bytes, void* stream);
+
 /* K2 -- all eigenpairs of the symmetric n x n G, eigenvalues descending,
  * first nvec eigenvectors in V.  Replaces scipy.linalg.eigh + reversal
  * (pod.py:329-331, 386-388).  Parallel two-sided block Jacobi; synchronises

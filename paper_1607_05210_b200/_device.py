@@ -32,6 +32,11 @@ DRIFT_TOL = 1e-8          # pod.py:247
 JACOBI_TOL_REL = 2.0 ** -52
 JACOBI_TOL_ABS = 16 * 2.0 ** -52  # absolute off-diagonal trigger, x max|g_ii| (Gram rounding floor)
 JACOBI_MAX_SWEEPS = 60
+# eigensolver: "pcjacobi" = pivoted-Cholesky preconditioned block Jacobi (default),
+# "jacobi" = block Jacobi directly on the Gramian (kept for comparison)
+import os as _os
+EIG_METHOD = _os.environ.get("HP_EIG_METHOD", "pcjacobi")
+PSTRF_TOL = float(_os.environ.get("HP_PSTRF_TOL", str(2.0 ** -52)))  # stop pivoting at u * max|G_ii|
 
 
 class Profiler:
@@ -288,43 +293,86 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     return G, total, keep
 
 
-def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
-                       want_right: bool, sqrt_w=None) -> NodeOutput:
-    """pod.py:278-293 on the device: eigensolve, truncation, reconstruction,
-    drift check + re-orthonormalisation, sign convention."""
+def _syev(G: DevMat, n: int, st):
     lib = N.load()
-    st = _stream()
-    lam = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
-    V = DevMat.empty(m, m)
-    ws = _ws(lib.hp_syev_workspace_bytes(m))
+    lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    V = DevMat.empty(n, n)
+    ws = _ws(lib.hp_syev_workspace_bytes(n))
     sweeps = ctypes.c_int(0)
     eflops = ctypes.c_double(0.0)
     ph = _phase("eigensolve")
     with ph:
-        N.check(lib.hp_syev(G.ptr, G.ld, m, lam.data_ptr(), V.ptr, V.ld, m, JACOBI_TOL_REL, JACOBI_TOL_ABS,
+        N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n, JACOBI_TOL_REL, JACOBI_TOL_ABS,
                             JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
                             ws.numel(), st), "eigensolve")
         ph.flops = eflops.value
-    del ws
+    return lam, V, sweeps.value
+
+
+def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
+                       want_right: bool, sqrt_w=None) -> NodeOutput:
+    """pod.py:278-293 on the device: eigensolve, truncation, reconstruction,
+    drift check + re-orthonormalisation, sign convention.
+
+    Eigensolve (default "pcjacobi"): G = L L^T by pivoted Cholesky (rows of L in
+    the original order), H = L^T L, H = W Lambda W^T by block Jacobi, and the
+    eigenvectors of G are V = L W Lambda^{-1/2}.  Same eigenpairs as
+    eigh(G) (pod.py:329), a handful of Jacobi sweeps instead of dozens."""
+    lib = N.load()
+    st = _stream()
+    Lf = None
+    if EIG_METHOD == "pcjacobi" and m > 0:
+        Lf = DevMat.empty(m, m)
+        piv = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        rank = ctypes.c_int64(0)
+        ws = _ws(lib.hp_pstrf_workspace_bytes(m))
+        with _phase("pstrf", float(m) ** 3 / 3.0):
+            N.check(lib.hp_pstrf(G.ptr, G.ld, m, Lf.ptr, Lf.ld, piv.data_ptr(), PSTRF_TOL, ctypes.byref(rank),
+                                 ws.data_ptr(), ws.numel(), st), "pivoted Cholesky")
+        del ws
+        r = int(rank.value)
+        Lr = Lf.view_cols(0, r)
+        H = DevMat.empty(r, r)
+        if r:
+            ws = _ws(lib.hp_gram_workspace_bytes(m, r))
+            with _phase("gram", float(m) * r * (r + 1)):
+                N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
+                        "H = L^T L")
+            del ws
+        lam, W, sweeps = _syev(H, r, st)
+        nev = r
+    else:
+        lam, W, sweeps = _syev(G, m, st)
+        nev = m
     sig = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
     info = torch.empty(4, dtype=torch.float64, device="cuda")
     with _phase("truncate"):
-        N.check(lib.hp_truncate(lam.data_ptr(), m, float(eps), float(cutoff), m, sig.data_ptr(), info.data_ptr(),
-                                st), "truncate")
+        N.check(lib.hp_truncate(lam.data_ptr(), nev, float(eps), float(cutoff), m, sig.data_ptr(),
+                                info.data_ptr(), st), "truncate")
     lam_max, nkeep, n_modes, tail = info.cpu().tolist()
     nkeep, n_modes = int(nkeep), int(n_modes)
     if not (lam_max > 0.0):
         return NodeOutput(None, np.zeros(0), ones(0), 0.0,
                           DevMat.empty(m, 0) if want_right else None, lam_max, 0, 0.0, False,
-                          sweeps.value, m)
+                          sweeps, m)
     sig_dev = sig[:n_modes].clone()
     if n_modes == 0:
         return NodeOutput(DevMat.empty(d, 0), np.zeros(0), sig_dev, tail,
                           DevMat.empty(m, 0) if want_right else None, lam_max, nkeep, 0.0, False,
-                          sweeps.value, m)
+                          sweeps, m)
     vs, scale, m2, keep = _concat_parts(parts)
     assert m2 == m
-    Vn = V.view_cols(0, n_modes)
+    if Lf is not None:
+        # eigenvectors of G: V_N = L W_N / sigma_N   (G V = L (L^T L) W / sigma = L W Lambda / sigma)
+        Vn = DevMat.empty(m, n_modes)
+        ws = _ws(lib.hp_gemm_workspace_bytes(m, n_modes, nev, 0, 0))
+        with _phase("eigvec", 2.0 * m * nev * n_modes):
+            N.check(lib.hp_gemm(0, 1, m, n_modes, nev, Lf.view_cols(0, nev).vecset(), W.vecset(), 1.0, 0.0,
+                                Vn.ptr, Vn.ld, None, None, sig_dev.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(),
+                                st), "V = L W / sigma")
+        del ws, Lf
+    else:
+        Vn = W.view_cols(0, n_modes)
     if scale is not None:
         Vs = DevMat.empty(m, n_modes)
         N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
@@ -361,12 +409,12 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         N.check(lib.hp_scale(U.ptr, U.ld, d, n_modes, None, sqrt_w.data_ptr(), None, U.ptr, U.ld, st), "unweigh")
     R = None
     if want_right:
-        R = V.view_cols(0, n_modes).clone()
+        R = Vn.clone()
     with _phase("signs"):
         N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None,
                              R.ld if R is not None else 0, m if R is not None else 0, None, st), "signs")
     sig_host = sig_dev.cpu().numpy()
-    return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps.value, m)
+    return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps, m)
 
 
 def node_pod(parts: list[Part], d: int, eps: float, cutoff: float, want_right: bool, sqrt_w=None) -> NodeOutput:

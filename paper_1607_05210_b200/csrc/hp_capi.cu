@@ -45,6 +45,9 @@ int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const 
 int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st);
 int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, double* partial,
               cudaStream_t st);
+size_t pstrf_workspace_bytes(int64_t m);
+int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
+              int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st);
 
 static inline VecSet vs(const hp_vecset& v) { return VecSet{v.base, v.ld, v.table}; }
 
@@ -336,6 +339,14 @@ int hp_scale(const double* src, int64_t lds, int64_t rows, int64_t cols, const d
 
 int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, void* stream) {
   return finite_check_run(src, lds, rows, cols, bad, (cudaStream_t)stream);
+}
+
+size_t hp_pstrf_workspace_bytes(int64_t m) { return pstrf_workspace_bytes(m); }
+
+int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
+             int64_t* rank, void* ws, size_t ws_bytes, void* stream) {
+  HP_REQUIRE(m >= 0 && ldg >= m && ldl >= m, "hp_pstrf: bad dimensions");
+  return pstrf_run(G, ldg, m, L, ldl, piv, tol_rel, rank, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 size_t hp_sumsq_workspace_bytes(void) { return 1024 * sizeof(double); }

@@ -1,0 +1,271 @@
+// Pivoted Cholesky of the node Gramian: the preconditioner of the eigensolver.
+//
+// G (m x m, symmetric positive semi-definite up to rounding) is factored as
+// G = L L^T + E with complete diagonal pivoting, L (m x r) stored with its
+// rows in the ORIGINAL index order -- pivoting is bookkeeping only, nothing
+// is swapped.  The factorisation runs until the largest remaining pivot is
+// <= tol (E is then rounding noise below the Gramian cutoff of pod.py:284).
+//
+// Why: the eigenvalues of G are those of H = L^T L (r x r) and its
+// eigenvectors are V = L W Lambda^{-1/2} (W = eigenvectors of H).  H is
+// strongly graded (column norms of L follow the pivots), so two-sided Jacobi
+// on H converges in a handful of sweeps where Jacobi on G stalls at the
+// rounding floor -- the QR-preconditioning of Drmac & Veselic, applied to the
+// method of snapshots.
+//
+// Kernel structure, per panel of PB columns:
+//   pstrf_panel : cooperative persistent kernel (one CTA per SM).  For each
+//                 column j: grid-wide argmax of the running diagonal d
+//                 (ties -> smallest index), L[:, j] = (A[:, p] - L_panel L_panel[p]^T)
+//                 / sqrt(d_p) over the CTA's row slice, d -= L[:, j]^2.
+//                 Two grid.sync() per column.
+//   trailing    : A -= L_panel L_panel^T (full m x m, symmetric) on the DMMA
+//                 GEMM engine.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "hp_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hp {
+
+int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
+             double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
+             const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+
+namespace pc {
+
+constexpr int PB = 64;       // panel width
+constexpr int PT = 256;      // threads per CTA
+
+struct Params {
+  double* A;        // m x m working copy (trailing-updated), ld = lda
+  int64_t lda;
+  int64_t m;
+  double* L;        // m x m (first r columns used), ld = ldl
+  int64_t ldl;
+  double* d;        // running diagonal, -inf once pivoted
+  int* piv;         // piv[j] = original index of the j-th pivot
+  double* red_v;    // per-CTA argmax partials
+  int* red_i;
+  int* rank;        // device: number of columns factored so far (stops growing at tol)
+  double tol;
+  int k0, k1;       // panel columns [k0, k1)
+};
+
+__device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+__global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[PT / 32];
+  __shared__ int si[PT / 32];
+  __shared__ double s_dp;
+  __shared__ int s_p;
+  __shared__ double s_lp[PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nblk = gridDim.x;
+  // contiguous row slice of this CTA
+  const int64_t per = (p.m + nblk - 1) / nblk;
+  const int64_t r0 = blockIdx.x * per, r1 = min(p.m, r0 + per);
+
+  for (int j = p.k0; j < p.k1; ++j) {
+    // ---- argmax of the running diagonal over unpivoted rows
+    double bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int64_t i = r0 + tid; i < r1; i += PT) {
+      const double v = p.d[i];
+      if (better(v, (int)i, bv, bi)) {
+        bv = v;
+        bi = (int)i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      sv[warp] = bv;
+      si[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double cv = sv[0];
+      int ci = si[0];
+      for (int w = 1; w < PT / 32; ++w)
+        if (better(sv[w], si[w], cv, ci)) {
+          cv = sv[w];
+          ci = si[w];
+        }
+      p.red_v[blockIdx.x] = cv;
+      p.red_i[blockIdx.x] = ci;
+    }
+    grid.sync();
+    // every CTA reduces the partials redundantly (identical result everywhere)
+    if (tid == 0) {
+      double gv = -INFINITY;
+      int gi = 0x7fffffff;
+      for (int b = 0; b < (int)nblk; ++b)
+        if (better(p.red_v[b], p.red_i[b], gv, gi)) {
+          gv = p.red_v[b];
+          gi = p.red_i[b];
+        }
+      s_dp = gv;
+      s_p = gi;
+    }
+    __syncthreads();
+    const double dp = s_dp;
+    const int pv = s_p;
+    // factorisation finished: the remaining pivots are rounding noise.  The test is
+    // uniform across the grid (every CTA reduced the same partials); rank stays j.
+    if (!(dp > p.tol)) return;
+    const double ljj = sqrt(dp);
+    // L[p, t] for the panel columns so far (t in [k0, j))
+    for (int t = p.k0 + tid; t < j; t += PT) s_lp[t - p.k0] = p.L[(int64_t)t * p.ldl + pv];
+    __syncthreads();
+    // ---- column j over the CTA's rows
+    const double* acol = p.A + (int64_t)pv * p.lda;
+    for (int64_t i = r0 + tid; i < r1; i += PT) {
+      double li;
+      if (i == pv) {
+        li = ljj;
+      } else if (p.d[i] == -INFINITY) {
+        li = 0.0;  // already pivoted: L is lower triangular in pivot order
+      } else {
+        double s = acol[i];
+        for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
+        li = s / ljj;
+        p.d[i] -= li * li;
+      }
+      p.L[(int64_t)j * p.ldl + i] = li;
+    }
+    if (pv >= r0 && pv < r1 && tid == 0) {
+      p.d[pv] = -INFINITY;
+      p.piv[j] = pv;
+    }
+    if (blockIdx.x == 0 && tid == 0) *p.rank = j + 1;
+    grid.sync();
+  }
+}
+
+__global__ void diag_init(const double* G, int64_t ldg, int64_t m, double* A, int64_t lda, double* d) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * m) return;
+  const int64_t j = e / m, i = e % m;
+  const double v = G[j * ldg + i];
+  A[j * lda + i] = v;
+  if (i == j) d[i] = v;
+}
+
+__global__ void max_diag_kernel(const double* d, int64_t m, double* out) {
+  __shared__ double red[256];
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += 256) mx = fmax(mx, fabs(d[i]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+}  // namespace pc
+
+size_t pstrf_workspace_bytes(int64_t m) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const int64_t ld = (m + 1) & ~int64_t(1);
+  size_t o = al((size_t)ld * m * 8);          // A
+  o += al((size_t)m * 8);                       // d
+  o += al(2048 * 8) + al(2048 * 4) + al(64);    // partials + rank + scal
+  o += al(gemm_workspace_bytes(m, m, pc::PB, 1, 0));
+  return o;
+}
+
+// G (m x m) -> L (m x r, rows in original order), piv (r), rank r (host).
+// tol_rel: stop when the largest remaining pivot <= tol_rel * max_i |G_ii|.
+int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
+              int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace pc;
+  HP_REQUIRE(ws_bytes >= pstrf_workspace_bytes(m), "pstrf: workspace too small");
+  *rank_out = 0;
+  if (m == 0) return HP_OK;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const int64_t lda = (m + 1) & ~int64_t(1);
+  char* base = static_cast<char*>(ws);
+  size_t o = 0;
+  double* A = reinterpret_cast<double*>(base + o);
+  o += al((size_t)lda * m * 8);
+  double* d = reinterpret_cast<double*>(base + o);
+  o += al((size_t)m * 8);
+  double* red_v = reinterpret_cast<double*>(base + o);
+  o += al(2048 * 8);
+  int* red_i = reinterpret_cast<int*>(base + o);
+  o += al(2048 * 4);
+  int* rank = reinterpret_cast<int*>(base + o);
+  double* scal = reinterpret_cast<double*>(base + o + 16);
+  o += al(64);
+  void* gws = base + o;
+  const size_t gwsb = ws_bytes - o;
+
+  diag_init<<<(unsigned)ceil_div(m * m, 256), 256, 0, st>>>(G, ldg, m, A, lda, d);
+  HP_CHECK_LAUNCH("diag_init");
+  max_diag_kernel<<<1, 256, 0, st>>>(d, m, scal);
+  HP_CHECK_LAUNCH("max_diag");
+  HP_CHECK_CUDA(cudaMemsetAsync(rank, 0, sizeof(int), st));
+  double host_scal = 0.0;
+  HP_CHECK_CUDA(cudaMemcpyAsync(&host_scal, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+  HP_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (!(host_scal > 0.0)) return HP_OK;  // all-zero Gramian: rank 0
+
+  int dev = 0, nsm = 148, per_sm = 1;
+  HP_CHECK_CUDA(cudaGetDevice(&dev));
+  HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pstrf_panel, PT, 0));
+  const int rows_per_cta = 64;
+  int grid = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), ceil_div(m, rows_per_cta));
+  grid = std::max(1, std::min(grid, 2048));
+
+  Params p{};
+  p.A = A;
+  p.lda = lda;
+  p.m = m;
+  p.L = L;
+  p.ldl = ldl;
+  p.d = d;
+  p.piv = piv;
+  p.red_v = red_v;
+  p.red_i = red_i;
+  p.rank = rank;
+  p.tol = tol_rel * host_scal;
+  int host_rank = 0;
+  for (int64_t k0 = 0; k0 < m; k0 += PB) {
+    p.k0 = (int)k0;
+    p.k1 = (int)std::min<int64_t>(m, k0 + PB);
+    void* args[] = {&p};
+    HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel, grid, PT, args, 0, st));
+    count_launches(1);
+    HP_CHECK_CUDA(cudaMemcpyAsync(&host_rank, rank, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HP_CHECK_CUDA(cudaStreamSynchronize(st));
+    const int64_t done = host_rank;
+    if (done < p.k1 || done >= m) break;
+    // trailing update of the whole working matrix: A -= L_panel L_panel^T
+    VecSet a{L + k0 * ldl, ldl, nullptr};
+    int rc = gemm_run(false, false, m, m, p.k1 - k0, a, a, (ldl % 2 == 0), -1.0, 1.0, A, lda, nullptr, nullptr,
+                      nullptr, 1, 0, gws, gwsb, st);
+    if (rc) return rc;
+  }
+  *rank_out = host_rank;
+  return HP_OK;
+}
+
+}  // namespace hp
