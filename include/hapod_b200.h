@@ -121,12 +121,13 @@ size_t hp_drift_workspace_bytes(int64_t d, int64_t N);
 int hp_drift(const double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double* drift_out, void* ws,
              size_t ws_bytes, void* stream);
 
-/* K5b -- U <- Q factor of U (CholQR2, shifted CholQR3 on breakdown): the same
- * span and Gram-Schmidt column order as the MGS sweep of pod.py:227-237.
- * C = U^T U on entry (destroyed).  Synchronises the stream. */
+/* K5b -- U <- Q factor of U (CholQR: one pass when drift <= 1e-2, else
+ * CholQR2; shifted CholQR3 on breakdown; pass drift < 0 to force two passes):
+ * the same span and Gram-Schmidt column order as the MGS sweep of
+ * pod.py:227-237.  C = U^T U on entry (destroyed).  Synchronises the stream. */
 size_t hp_reortho_workspace_bytes(int64_t d, int64_t N);
-int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, int* passes_out,
-                        void* ws, size_t ws_bytes, void* stream);
+int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double drift,
+                        int* passes_out, void* ws, size_t ws_bytes, void* stream);
 
 /* K6 -- sign convention (pod.py:214-224): per column, the largest-|.| entry
  * (first index on ties) made positive; R (m_r x N, nullable) flipped alike;

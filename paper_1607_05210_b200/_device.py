@@ -398,10 +398,14 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     if drift > DRIFT_TOL:
         ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
         passes = ctypes.c_int(0)
-        # CholQR2: pass 1 reuses the drift Gram (U L^-T: d N^2), pass 2 = SYRK + U L^-T
-        with _phase("reortho", float(d) * n_modes * n_modes * 2 + float(d) * n_modes * (n_modes + 1)):
-            N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, ctypes.byref(passes),
+        # CholQR: pass 1 reuses the drift Gram (U L^-T: d N^2 flops); a second pass (SYRK + U L^-T)
+        # only when the drift says kappa(U) is not ~1
+        ph = _phase("reortho", float(d) * n_modes * n_modes)
+        with ph:
+            N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, drift, ctypes.byref(passes),
                                             ws.data_ptr(), ws.numel(), st), "re-orthonormalisation")
+            if passes.value > 1:
+                ph.flops += (passes.value - 1) * (float(d) * n_modes * n_modes + float(d) * n_modes * (n_modes + 1))
         del ws
         reorthed = True
     del C

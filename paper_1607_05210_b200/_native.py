@@ -52,7 +52,7 @@ _SIGNATURES = {
     "hp_drift_workspace_bytes": (c_size, [c_i64, c_i64]),
     "hp_drift": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_size, c_vp]),
     "hp_reortho_workspace_bytes": (c_size, [c_i64, c_i64]),
-    "hp_reorthonormalize": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, ctypes.POINTER(c_int),
+    "hp_reorthonormalize": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_dbl, ctypes.POINTER(c_int),
                                     c_vp, c_size, c_vp]),
     "hp_signs": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "hp_transpose_rm_to_cm": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),

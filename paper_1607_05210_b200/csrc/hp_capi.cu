@@ -105,6 +105,9 @@ static int cholqr_pass(const double* X, int64_t ldx, int64_t d, int64_t N, doubl
   return rc;
 }
 
+// drift below which one CholQR pass is already orthonormal to the rounding level
+static constexpr double kSinglePassDrift = 1e-2;
+
 static int gram_sym(const double* X, int64_t ldx, int64_t d, int64_t N, double* C, int64_t ldc, void* ws,
                     size_t wsb, cudaStream_t st) {
   VecSet a{X, ldx, nullptr};
@@ -248,11 +251,13 @@ size_t hp_reortho_workspace_bytes(int64_t d, int64_t N) {
   return reortho_layout(d, N, ldx).total;
 }
 
-// U <- Q of the QR factorisation of U (CholQR2; shifted CholQR3 when the
-// first Cholesky breaks down).  C holds U^T U on entry (from hp_drift) and is
-// destroyed.  Same span and column order as the MGS sweep of pod.py:227-237.
-int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, int* passes_out,
-                        void* ws, size_t ws_bytes, void* stream) {
+// U <- Q of the QR factorisation of U: CholQR (one pass when the drift is
+// small enough that kappa(U)^2 ~ 1 + 2 drift makes a single pass accurate to
+// the rounding level, else CholQR2; shifted CholQR3 when the first Cholesky
+// breaks down).  C holds U^T U on entry (from hp_drift) and is destroyed.
+// Same span and column order as the MGS sweep of pod.py:227-237.
+int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double drift,
+                        int* passes_out, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (passes_out) *passes_out = 0;
   if (N == 0) return HP_OK;
@@ -303,6 +308,21 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
     passes += 1;
   }
   passes += 1;
+  const bool single = (passes == 1) && (drift >= 0.0) && (drift <= kSinglePassDrift);
+  if (single) {
+    if (!rc) rc = scale_run(X, ldx, d, N, nullptr, nullptr, nullptr, U, ldu, st);
+    if (passes_out) *passes_out = passes;
+    if (!rc) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        set_error(std::string("reortho: ") + cudaGetErrorString(e));
+        rc = HP_ECUDA;
+      }
+    }
+    cudaFreeHost(hinfo);
+    cudaFreeHost(htrace);
+    return rc;
+  }
   // second pass: X -> U
   if (!rc) rc = gram_sym(X, ldx, d, N, A, ldn, gws, gwsb, st);
   if (!rc) rc = cholqr_pass(X, ldx, d, N, A, ldn, U, ldu, L, base, ws_bytes, st, &hinfo[0]);

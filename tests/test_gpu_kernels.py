@@ -178,8 +178,9 @@ def test_signs_and_reortho():
     assert float(drift.item()) == pytest.approx(ref_drift, rel=1e-6)
     w = ws(lib.hp_reortho_workspace_bytes(d, n))
     passes = ctypes.c_int(0)
-    N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n, C.ptr, C.ld, ctypes.byref(passes), w.data_ptr(), w.numel(),
-                                    st()), "reortho")
+    N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n, C.ptr, C.ld, float(drift.item()), ctypes.byref(passes),
+                                    w.data_ptr(), w.numel(), st()), "reortho")
+    assert passes.value == 1  # drift ~1e-4: one CholQR pass
     qq = U.to_numpy()
     assert np.max(np.abs(qq.T @ qq - np.eye(n))) < 1e-13
     # same Q as Gram-Schmidt (positive diagonal R)
@@ -190,3 +191,28 @@ def test_signs_and_reortho():
     s = U.to_numpy()
     pick = np.argmax(np.abs(s), axis=0)
     assert np.all(s[pick, np.arange(n)] > 0)
+
+
+@pytest.mark.parametrize("scale", [1e-1, 3e-2])
+def test_reortho_two_pass_and_shifted(scale):
+    rng = np.random.default_rng(4)
+    d, n = 3000, 150
+    q, _ = np.linalg.qr(rng.standard_normal((d, n)))
+    # graded columns: kappa ~ 1e6 (scale 1e-1) .. forces CholQR2 / shifted CholQR3
+    u = q @ (np.eye(n) + scale * rng.standard_normal((n, n))) * np.logspace(0, -6 * (scale > 5e-2), n)[None, :]
+    U = D.upload(u)
+    C = D.DevMat.empty(n, n)
+    drift = torch.zeros(1, dtype=torch.float64, device="cuda")
+    w = ws(lib.hp_drift_workspace_bytes(d, n))
+    N.check(lib.hp_drift(U.ptr, U.ld, d, n, C.ptr, C.ld, drift.data_ptr(), w.data_ptr(), w.numel(), st()), "drift")
+    w = ws(lib.hp_reortho_workspace_bytes(d, n))
+    passes = ctypes.c_int(0)
+    N.check(lib.hp_reorthonormalize(U.ptr, U.ld, d, n, C.ptr, C.ld, float(drift.item()), ctypes.byref(passes),
+                                    w.data_ptr(), w.numel(), st()), "reortho")
+    qq = U.to_numpy()
+    assert passes.value >= 2
+    assert np.max(np.abs(qq.T @ qq - np.eye(n))) < 1e-12
+    qr_q, r = np.linalg.qr(u)
+    qr_q = qr_q * np.sign(np.diag(r))[None, :]
+    # same span (Q unique up to rounding ~ u kappa)
+    assert np.linalg.norm(qr_q - qq @ (qq.T @ qr_q)) < 1e-6
