@@ -87,7 +87,7 @@ int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F
  * The eigenvalues of G are those of H = L^T L; its eigenvectors
  * V = L W Lambda^{-1/2} (W = eigenvectors of H).  piv (device, m ints)
  * receives the pivot order; rank (host) receives r.  Synchronises once per
- * 64-column panel. */
+ * 128-column panel. */
 size_t hp_pstrf_workspace_bytes(int64_t m);
 int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
              int64_t* rank, void* ws, size_t ws_bytes, void* stream);
@@ -121,7 +121,7 @@ size_t hp_drift_workspace_bytes(int64_t d, int64_t N);
 int hp_drift(const double* U, int64_t ldu, int64_t d, int64_t N, double* C, int64_t ldc, double* drift_out, void* ws,
              size_t ws_bytes, void* stream);
 
-/* K5b -- U <- Q factor of U (CholQR: one pass when drift <= 1e-2, else
+/* K5b -- U <- Q factor of U (CholQR: one pass when drift <= 1e-1, else
  * CholQR2; shifted CholQR3 on breakdown; pass drift < 0 to force two passes):
  * the same span and Gram-Schmidt column order as the MGS sweep of
  * pod.py:227-237.  C = U^T U on entry (destroyed).  Synchronises the stream. */

@@ -106,7 +106,7 @@ static int cholqr_pass(const double* X, int64_t ldx, int64_t d, int64_t N, doubl
 }
 
 // drift below which one CholQR pass is already orthonormal to the rounding level
-static constexpr double kSinglePassDrift = 1e-2;
+static constexpr double kSinglePassDrift = 1e-1;
 
 static int gram_sym(const double* X, int64_t ldx, int64_t d, int64_t N, double* C, int64_t ldc, void* ws,
                     size_t wsb, cudaStream_t st) {

@@ -96,10 +96,52 @@ __device__ __forceinline__ bool needs_rotation(double aij, double aii, double aj
   return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj));
 }
 
+// C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
+//  transX = false: X(m,k) at X[k*TS + m];  transX = true: X(m,k) = X[m*TS + k]
+// 8 warps: warp w owns rows (w&3)*16..+16 and cols (w>>2)*32..+32.
+template <bool TRANSX, int SX = TS, int SY = TS>
+__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&acc)[2][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < PS; k0 += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int m = r0 + i * 8 + g, kk = k0 + t;
+      a[i] = TRANSX ? X[m * SX + kk] : X[kk * SX + m];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Y[(c0 + j * 8 + g) * SY + k0 + t];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+  }
+}
+
+template <int SC = TS>
+__device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C[(c0 + j * 8 + 2 * t + e) * SC + r0 + i * 8 + g] = acc[i][j][e];
+}
+
 __global__ void __launch_bounds__(LT) jac_local(Params p) {
   extern __shared__ double sm[];
   double* A = sm;               // PS x LS (A[i*LS + j] = a_ij, symmetric)
-  double* Wl = A + PS * LS;     // PS x LS (Wl[i*LS + j] = w_ij)
+  double* Wl = A + PS * LS;     // PS x LS, column-major: Wl[j*LS + i] = w_ij
   __shared__ double cs[PS / 2], sn[PS / 2], tt[PS / 2];
   __shared__ int pi[PS / 2], pj[PS / 2], rot[PS / 2];
   __shared__ int any_rot;
@@ -219,9 +261,9 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
         if (!rot[Q]) continue;
         const int i2 = pi[Q], j2 = pj[Q];
         const double c = cs[Q], s = sn[Q];
-        const double wi = Wl[r * LS + i2], wj = Wl[r * LS + j2];
-        Wl[r * LS + i2] = c * wi - s * wj;
-        Wl[r * LS + j2] = s * wi + c * wj;
+        const double wi = Wl[i2 * LS + r], wj = Wl[j2 * LS + r];
+        Wl[i2 * LS + r] = c * wi - s * wj;
+        Wl[j2 * LS + r] = s * wi + c * wj;
       }
       __syncthreads();
     }
@@ -240,25 +282,38 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     sperm[r] = tid;
   }
   __syncthreads();
-  // one Bjorck step: E = I - W^T W ; W <- W + W E / 2   (result staged in A's buffer)
+  // one Bjorck step on DMMA (warps 0-7), W column-major in Wl:
+  //   E = W^T W - I ;  W_new = W - W E / 2     (staged column-major in A's buffer)
   double* E = Wl + PS * LS;
-  for (int e = tid; e < PS * PS; e += LT) {
-    const int i = e / PS, j = e % PS;
-    double sdot = 0.0;
-    for (int q = 0; q < PS; ++q) sdot += Wl[q * LS + i] * Wl[q * LS + j];
-    E[i * LS + j] = (i == j ? 1.0 : 0.0) - sdot;
+  {
+    double acc[2][4][2];
+    const int warp = tid >> 5;
+    if (warp < 8) mm64<true, LS, LS>(Wl, Wl, acc);   // A(m,k) = Wl[m*LS+k] = W(k,m), B(k,n) = Wl[n*LS+k] = W(k,n)
+    __syncthreads();
+    if (warp < 8) store_acc<LS>(E, acc);
+    __syncthreads();
+    for (int e = tid; e < PS; e += LT) E[e * LS + e] -= 1.0;
+    __syncthreads();
+    if (warp < 8) mm64<false, LS, LS>(Wl, E, acc);  // A(m,k) = Wl[k*LS+m] = W(m,k), B(k,n) = E(k,n)
+    __syncthreads();
+    if (warp < 8) {
+      const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+      const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int m = r0 + i * 8 + g, n = c0 + j * 8 + 2 * t + e2;
+            A[n * LS + m] = Wl[n * LS + m] - 0.5 * acc[i][j][e2];
+          }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = tid; e < PS * PS; e += LT) {
-    const int r = e / PS, j = e % PS;
-    double sdot = 0.0;
-    for (int q = 0; q < PS; ++q) sdot += Wl[r * LS + q] * E[q * LS + j];
-    A[r * LS + j] = Wl[r * LS + j] + 0.5 * sdot;
-  }
-  __syncthreads();
   for (int e = tid; e < PS * PS; e += LT) {
     const int j = e / PS, i = e % PS;
-    p.W[(int64_t)k * PS * PS + j * PS + i] = A[i * LS + sperm[j]];
+    p.W[(int64_t)k * PS * PS + j * PS + i] = A[sperm[j] * LS + i];
   }
   if (tid == 0) {
     p.flags[k] = 1;
@@ -266,51 +321,27 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
   }
 }
 
-// C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
-//  transX = false: X(m,k) at X[k*TS + m];  transX = true: X(m,k) = X[m*TS + k]
-// 8 warps: warp w owns rows (w&3)*16..+16 and cols (w>>2)*32..+32.
-template <bool TRANSX>
-__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&acc)[2][4][2]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 4
-  for (int k0 = 0; k0 < PS; k0 += 4) {
-    double a[2], b[4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int m = r0 + i * 8 + g, kk = k0 + t;
-      a[i] = TRANSX ? X[m * TS + kk] : X[kk * TS + m];
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = Y[(c0 + j * 8 + g) * TS + k0 + t];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+// async 16-byte copies: a 64x64 column-major W (contiguous) into smem stride TS
+__device__ __forceinline__ void load_w(double* dst, const double* W) {
+  for (int e = threadIdx.x; e < PS * PS / 2; e += AT) {
+    const int j = e / (PS / 2), i = (e % (PS / 2)) * 2;
+    cp_async_16(dst + j * TS + i, W + j * PS + i, 16);
   }
 }
 
-__device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) C[(c0 + j * 8 + 2 * t + e) * TS + r0 + i * 8 + g] = acc[i][j][e];
+// async gather of the 64x64 tile M[I_rows, I_cols] (column-major, leading dimension ld)
+__device__ __forceinline__ void load_tile(double* dst, const double* M, int64_t ld, int rp, int rq, int cp_, int cq) {
+  for (int e = threadIdx.x; e < PS * PS / 2; e += AT) {
+    const int j = e / (PS / 2), i = (e % (PS / 2)) * 2;
+    const int64_t col = local_index(cp_, cq, j), row = local_index(rp, rq, i);
+    cp_async_16(dst + j * TS + i, M + col * ld + row, 16);
+  }
 }
 
-__device__ __forceinline__ void load_w(double* dst, const double* W) {
-  for (int e = threadIdx.x; e < PS * PS; e += AT) {
-    const int j = e / PS, i = e % PS;
-    dst[j * TS + i] = W[e];
+__device__ __forceinline__ void load_slab(double* dst, const double* V, int64_t ld, int64_t row0, int cp_, int cq) {
+  for (int e = threadIdx.x; e < PS * PS / 2; e += AT) {
+    const int j = e / (PS / 2), i = (e % (PS / 2)) * 2;
+    cp_async_16(dst + j * TS + i, V + local_index(cp_, cq, j) * ld + row0 + i, 16);
   }
 }
 
@@ -334,13 +365,12 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
     int pp, pq, qp, qq;
     block_pair(p, P, pp, pq);
     block_pair(p, Q, qp, qq);
-    for (int e = threadIdx.x; e < PS * PS; e += AT) {
-      const int j = e / PS, i = e % PS;
-      X[j * TS + i] = p.G[local_index(qp, qq, j) * p.np + local_index(pp, pq, i)];
-    }
+    load_tile(X, p.G, p.np, pp, pq, qp, qq);
     if (fQ) load_w(WQ, p.W + (int64_t)Q * PS * PS);
     if (fP) load_w(WP, p.W + (int64_t)P * PS * PS);
+    cp_async_commit();
     if (threadIdx.x == 0) atomicAdd(p.mm_count, (unsigned long long)(fP + fQ));
+    cp_async_wait<0>();
     __syncthreads();
     if (fQ) {
       mm64<false>(X, WQ, acc);  // X W_Q
@@ -380,12 +410,11 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   if (!p.flags[Q]) return;
   int qp, qq;
   block_pair(p, Q, qp, qq);
-  for (int e = threadIdx.x; e < PS * PS; e += AT) {
-    const int j = e / PS, i = e % PS;
-    X[j * TS + i] = p.V[local_index(qp, qq, j) * p.np + rc * PS + i];
-  }
+  load_slab(X, p.V, p.np, rc * PS, qp, qq);
   load_w(WQ, p.W + (int64_t)Q * PS * PS);
+  cp_async_commit();
   if (threadIdx.x == 0) atomicAdd(p.mm_count, 1ull);
+  cp_async_wait<0>();
   __syncthreads();
   mm64<false>(X, WQ, acc);
   __syncthreads();

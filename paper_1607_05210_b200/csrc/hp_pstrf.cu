@@ -39,7 +39,7 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_uppe
 
 namespace pc {
 
-constexpr int PB = 64;       // panel width
+constexpr int PB = 128;      // panel width
 constexpr int PT = 256;      // threads per CTA
 
 struct Params {
@@ -110,17 +110,31 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
       p.red_i[blockIdx.x] = ci;
     }
     grid.sync();
-    // every CTA reduces the partials redundantly (identical result everywhere)
-    if (tid == 0) {
+    // every CTA reduces the partials redundantly (identical result everywhere): warp 0,
+    // lane-strided loads + shuffle reduction (the partials live in L2)
+    if (warp == 0) {
       double gv = -INFINITY;
       int gi = 0x7fffffff;
-      for (int b = 0; b < (int)nblk; ++b)
-        if (better(p.red_v[b], p.red_i[b], gv, gi)) {
-          gv = p.red_v[b];
-          gi = p.red_i[b];
+      for (int b = lane; b < (int)nblk; b += 32) {
+        const double v = __ldcg(p.red_v + b);
+        const int ii = __ldcg(p.red_i + b);
+        if (better(v, ii, gv, gi)) {
+          gv = v;
+          gi = ii;
         }
-      s_dp = gv;
-      s_p = gi;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        if (better(ov, oi, gv, gi)) {
+          gv = ov;
+          gi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_dp = gv;
+        s_p = gi;
+      }
     }
     __syncthreads();
     const double dp = s_dp;

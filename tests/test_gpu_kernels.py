@@ -193,13 +193,13 @@ def test_signs_and_reortho():
     assert np.all(s[pick, np.arange(n)] > 0)
 
 
-@pytest.mark.parametrize("scale", [1e-1, 3e-2])
-def test_reortho_two_pass_and_shifted(scale):
+@pytest.mark.parametrize("scale,graded", [(1e-1, True), (8e-2, False)])
+def test_reortho_two_pass_and_shifted(scale, graded):
     rng = np.random.default_rng(4)
     d, n = 3000, 150
     q, _ = np.linalg.qr(rng.standard_normal((d, n)))
     # graded columns: kappa ~ 1e6 (scale 1e-1) .. forces CholQR2 / shifted CholQR3
-    u = q @ (np.eye(n) + scale * rng.standard_normal((n, n))) * np.logspace(0, -6 * (scale > 5e-2), n)[None, :]
+    u = q @ (np.eye(n) + scale * rng.standard_normal((n, n))) * np.logspace(0, -6 * graded, n)[None, :]
     U = D.upload(u)
     C = D.DevMat.empty(n, n)
     drift = torch.zeros(1, dtype=torch.float64, device="cuda")
