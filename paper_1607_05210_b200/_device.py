@@ -37,6 +37,15 @@ JACOBI_MAX_SWEEPS = 60
 import os as _os
 EIG_METHOD = _os.environ.get("HP_EIG_METHOD", "pcjacobi")
 PSTRF_TOL = float(_os.environ.get("HP_PSTRF_TOL", str(2.0 ** -52)))  # stop pivoting at u * max|G_ii|
+# Rayleigh-Ritz polish of the preconditioned eigenpairs against G itself (restores LAPACK-class
+# accuracy of the eigenvalues at the Gram cutoff): eigenpairs with lambda above
+# POLISH_FACTOR * cutoff * lambda_max * m are re-solved in their own span.
+POLISH = _os.environ.get("HP_EIG_POLISH", "1") != "0"
+KEEP_SPECTRUM = False   # diagnostics: keep the last node's eigenvalues in LAST_SPECTRUM
+LAST_SPECTRUM: list = []
+POLISH_FACTOR = float(_os.environ.get("HP_EIG_POLISH_FACTOR", "1e-2"))
+POLISH_TOL_REL = float(_os.environ.get("HP_EIG_POLISH_TOL_REL", str(2.0 ** -52)))
+POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
 
 
 class Profiler:
@@ -293,16 +302,18 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     return G, total, keep
 
 
-def _syev(G: DevMat, n: int, st):
+def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0):
     lib = N.load()
     lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
     V = DevMat.empty(n, n)
     ws = _ws(lib.hp_syev_workspace_bytes(n))
     sweeps = ctypes.c_int(0)
     eflops = ctypes.c_double(0.0)
-    ph = _phase("eigensolve")
+    ph = _phase(name)
     with ph:
-        N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n, JACOBI_TOL_REL, JACOBI_TOL_ABS,
+        N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n,
+                            JACOBI_TOL_REL if tol_rel is None else tol_rel,
+                            JACOBI_TOL_ABS if tol_abs is None else tol_abs, float(keep_floor),
                             JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
                             ws.numel(), st), "eigensolve")
         ph.flops = eflops.value
@@ -321,6 +332,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     lib = N.load()
     st = _stream()
     Lf = None
+    basis, divide = None, False
     if EIG_METHOD == "pcjacobi" and m > 0:
         Lf = DevMat.empty(m, m)
         piv = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
@@ -341,14 +353,68 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
             del ws
         lam, W, sweeps = _syev(H, r, st)
         nev = r
+        basis, divide = Lf, True
+        if POLISH and r:
+            # K = #{lambda_H >= POLISH_FACTOR * cutoff * lambda_max * m}; sig = sqrt(lambda_H[:K])
+            sig_h = torch.empty(r, dtype=torch.float64, device="cuda")
+            info_h = torch.empty(4, dtype=torch.float64, device="cuda")
+            N.check(lib.hp_truncate(lam.data_ptr(), r, 0.0, float(cutoff) * POLISH_FACTOR, m, sig_h.data_ptr(),
+                                    info_h.data_ptr(), st), "polish count")
+            lam_max_h, K = float(info_h[0].item()), int(info_h[1].item())
+            if K:
+                # Q0 = L W_K Lambda_K^{-1/2}: approximate eigenvectors of G from the preconditioned solve.
+                # One subspace-iteration step X = G Q0 Lambda_K^{-1} damps the components along
+                # eigenvectors outside span(Q0) (left there by the Cholesky backward error) by
+                # lambda_j / lambda_i; CholQR keeps the descending order; Rayleigh-Ritz on
+                # G2 = X^T G X then resolves the mixing inside the span.
+                ws = _ws(max(lib.hp_gemm_workspace_bytes(m, K, r, 0, 0), lib.hp_gemm_workspace_bytes(m, K, m, 0, 0),
+                             lib.hp_gemm_workspace_bytes(K, K, m, 1, 0)))
+                with _phase("polish", 2.0 * m * r * K + 4.0 * m * m * K + 2.0 * m * K * K + float(m) * K * (K + 1)):
+                    Q0 = DevMat.empty(m, K)
+                    N.check(lib.hp_gemm(0, 1, m, K, r, Lr.vecset(), W.vecset(), 1.0, 0.0, Q0.ptr, Q0.ld, None, None,
+                                        sig_h.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "Q0 = L W / sigma")
+                    X = DevMat.empty(m, K)
+                    N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), Q0.vecset(), 1.0, 0.0, X.ptr, X.ld, None, None,
+                                        lam.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "X = G Q0 / lambda")
+                    del Q0
+                    C = DevMat.empty(K, K)
+                    drift_q = torch.zeros(1, dtype=torch.float64, device="cuda")
+                    N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_q.data_ptr(), ws.data_ptr(),
+                                         ws.numel(), st), "X^T X")
+                    rws = _ws(lib.hp_reortho_workspace_bytes(m, K))
+                    passes = ctypes.c_int(0)
+                    N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, float(drift_q.item()),
+                                                    ctypes.byref(passes), rws.data_ptr(), rws.numel(), st),
+                            "orthonormalise X")
+                    del rws, C
+                    T = DevMat.empty(m, K)
+                    N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), X.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None,
+                                        None, 0, 0, ws.data_ptr(), ws.numel(), st), "T = G X")
+                    G2 = DevMat.empty(K, K)
+                    N.check(lib.hp_gemm(1, 1, K, K, m, X.vecset(), T.vecset(), 1.0, 0.0, G2.ptr, G2.ld, None, None,
+                                        None, 1, 0, ws.data_ptr(), ws.numel(), st), "G2 = X^T G X")
+                    del T, ws
+                # G2 is nearly diagonal and graded: relative criterion, but never rotate two
+                # eigenvalues that are both below a tenth of the Gram cutoff (pod.py:284)
+                floor = 0.1 * float(cutoff) * lam_max_h * m
+                lam, W, sweeps2 = _syev(G2, K, st, "eigensolve_polish", tol_rel=POLISH_TOL_REL,
+                                        tol_abs=POLISH_TOL_ABS, keep_floor=floor)
+                sweeps += sweeps2
+                nev = K
+                basis, divide = X, False
+                del G2, Lf
+                Lf = None
     else:
         lam, W, sweeps = _syev(G, m, st)
         nev = m
+        basis, divide = None, False
     sig = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
     info = torch.empty(4, dtype=torch.float64, device="cuda")
     with _phase("truncate"):
         N.check(lib.hp_truncate(lam.data_ptr(), nev, float(eps), float(cutoff), m, sig.data_ptr(),
                                 info.data_ptr(), st), "truncate")
+    if KEEP_SPECTRUM:
+        LAST_SPECTRUM[:] = [lam[:nev].cpu().numpy()]
     lam_max, nkeep, n_modes, tail = info.cpu().tolist()
     nkeep, n_modes = int(nkeep), int(n_modes)
     if not (lam_max > 0.0):
@@ -362,15 +428,16 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                           sweeps, m)
     vs, scale, m2, keep = _concat_parts(parts)
     assert m2 == m
-    if Lf is not None:
-        # eigenvectors of G: V_N = L W_N / sigma_N   (G V = L (L^T L) W / sigma = L W Lambda / sigma)
+    if basis is not None:
+        # eigenvectors of G: V_N = L W_N / sigma_N  (G V = L (L^T L) W / sigma = L W Lambda / sigma), or,
+        # after the polish, V_N = Q W_N with Q the orthonormal Ritz basis
         Vn = DevMat.empty(m, n_modes)
         ws = _ws(lib.hp_gemm_workspace_bytes(m, n_modes, nev, 0, 0))
         with _phase("eigvec", 2.0 * m * nev * n_modes):
-            N.check(lib.hp_gemm(0, 1, m, n_modes, nev, Lf.view_cols(0, nev).vecset(), W.vecset(), 1.0, 0.0,
-                                Vn.ptr, Vn.ld, None, None, sig_dev.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(),
-                                st), "V = L W / sigma")
-        del ws, Lf
+            N.check(lib.hp_gemm(0, 1, m, n_modes, nev, basis.view_cols(0, nev).vecset(), W.vecset(), 1.0, 0.0,
+                                Vn.ptr, Vn.ld, None, None, sig_dev.data_ptr() if divide else None, 0, 0,
+                                ws.data_ptr(), ws.numel(), st), "eigenvectors of G")
+        del ws, basis
     else:
         Vn = W.view_cols(0, n_modes)
     if scale is not None:

@@ -65,6 +65,7 @@ struct Params {
   unsigned long long* mm_count;  // 64x64x64 DMMA products performed by jac_apply (flop accounting)
   const double* scal; // scal[0] = max |g_ii| of the input
   double tol_rel, tol_abs;
+  double keep_floor;  // pairs whose diagonal entries are both below this never rotate
   int max_local_sweeps;
 };
 
@@ -91,9 +92,10 @@ __device__ __forceinline__ int64_t local_index(int bp, int bq, int i) {
   return i < BW ? (int64_t)bp * BW + i : (int64_t)bq * BW + (i - BW);
 }
 
-__device__ __forceinline__ bool needs_rotation(double aij, double aii, double ajj, double tr, double ta) {
+__device__ __forceinline__ bool needs_rotation(double aij, double aii, double ajj, double tr, double ta,
+                                               double floor_ = 0.0) {
   const double a = fabs(aij);
-  return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj));
+  return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj)) && (floor_ <= 0.0 || fmax(aii, ajj) >= floor_);
 }
 
 // C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
@@ -140,41 +142,44 @@ __device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2
 
 __global__ void __launch_bounds__(LT) jac_local(Params p) {
   extern __shared__ double sm[];
-  double* A = sm;               // PS x LS (A[i*LS + j] = a_ij, symmetric)
-  double* Wl = A + PS * LS;     // PS x LS, column-major: Wl[j*LS + i] = w_ij
-  __shared__ double cs[PS / 2], sn[PS / 2], tt[PS / 2];
-  __shared__ int pi[PS / 2], pj[PS / 2], rot[PS / 2];
-  __shared__ int any_rot;
+  // A is double-buffered (each rotation step reads one copy and writes the other, so one
+  // barrier per step suffices); W is column-major (Wl[j*LS + i] = w_ij) and its rows are
+  // owned by warps (row % 16 == warp), so W needs only __syncwarp between steps.
+  double* Acur = sm;
+  double* Anx = sm + PS * LS;
+  double* Wl = sm + 2 * PS * LS;
+  __shared__ int sperm[PS];
 
   const int k = blockIdx.x;
   int bp, bq;
   block_pair(p, k, bp, bq);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double tr = p.tol_rel, ta = p.tol_abs * p.scal[0];
-  // local floor: entries below u*max|g_ii| are rounding noise -- do not chase them
-  const double tloc = 2.220446049250313e-16 * p.scal[0];
+  // local floor: with an absolute trigger, entries below u*max|g_ii| are rounding noise -- do
+  // not chase them; with a relative trigger (tol_abs tiny) the local solve follows it
+  const double tloc = fmin(2.220446049250313e-16 * p.scal[0], ta);
 
   for (int e = tid; e < PS * PS; e += LT) {
     const int j = e / PS, i = e % PS;
-    A[i * LS + j] = p.G[local_index(bp, bq, j) * p.np + local_index(bp, bq, i)];
+    Acur[i * LS + j] = p.G[local_index(bp, bq, j) * p.np + local_index(bp, bq, i)];
   }
   __syncthreads();
-  // anything to do?  (absolute trigger: tol_abs * max|g_ii|)
+  // anything to do?  |g_ij| > max(tol_abs * max|g_ii|, tol_rel * sqrt|g_ii g_jj|)
   int mine = 0;
   double moff = 0.0;
   for (int e = tid; e < PS * PS; e += LT) {
     const int i = e / PS, j = e % PS;
     if (i < j) {
-      const double a = fabs(A[i * LS + j]);
-      moff = fmax(moff, a);
-      if (a > ta) mine = 1;
+      const double aij = Acur[i * LS + j];
+      moff = fmax(moff, fabs(aij));
+      if (needs_rotation(aij, Acur[i * LS + i], Acur[j * LS + j], tr, ta, p.keep_floor)) mine = 1;
     }
   }
   {
     // sweep-level maximum off-diagonal ratio (non-negative doubles order like their bits)
     double r = moff / p.scal[0];
     for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
-    if ((tid & 31) == 0 && r > 0.0)
+    if (lane == 0 && r > 0.0)
       atomicMax(reinterpret_cast<unsigned long long*>(p.maxoff), (unsigned long long)__double_as_longlong(r));
   }
   if (!__syncthreads_or(mine)) {
@@ -182,67 +187,63 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     return;
   }
   for (int e = tid; e < PS * PS; e += LT) {
-    const int i = e / PS, j = e % PS;
-    Wl[i * LS + j] = (i == j) ? 1.0 : 0.0;
+    const int j = e / PS, i = e % PS;
+    Wl[j * LS + i] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
 
   for (int sweep = 0; sweep < p.max_local_sweeps; ++sweep) {
-    if (tid == 0) any_rot = 0;
-    __syncthreads();
+    int rotated = 0;
     for (int step = 0; step < PS - 1; ++step) {
-      if (tid < PS / 2) {
-        int a, b;
-        circle_pair(PS, step, tid, a, b);
-        const double aii = A[a * LS + a], ajj = A[b * LS + b], aij = A[a * LS + b];
-        int r = needs_rotation(aij, aii, ajj, tr, tloc);
-        double c = 1.0, s = 0.0, t = 0.0;
-        if (r) {
-          const double theta = (ajj - aii) / (2.0 * aij);
-          if (fabs(theta) > 1e150) {
-            t = 0.5 / theta;
-          } else {
-            t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          }
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = t * c;
-          any_rot = 1;
+      // rotation of pair `lane` (computed redundantly by every warp: no broadcast, no barrier)
+      int a, b;
+      circle_pair(PS, step, lane, a, b);
+      const double aii = Acur[a * LS + a], ajj = Acur[b * LS + b], aij = Acur[a * LS + b];
+      const int r = needs_rotation(aij, aii, ajj, tr, tloc, p.keep_floor);
+      double c = 1.0, s = 0.0, t = 0.0;
+      if (r) {
+        const double theta = (ajj - aii) / (2.0 * aij);
+        if (fabs(theta) > 1e150) {
+          t = 0.5 / theta;
+        } else {
+          t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
         }
-        cs[tid] = c;
-        sn[tid] = s;
-        tt[tid] = t;
-        pi[tid] = a;
-        pj[tid] = b;
-        rot[tid] = r;
+        c = rsqrt(1.0 + t * t);
+        s = t * c;
       }
-      __syncthreads();
-      // A <- R^T A R, one 2x2 block per (row pair, column pair)
-      for (int e = tid; e < (PS / 2) * (PS / 2); e += LT) {
-        const int P = e / (PS / 2), Q = e % (PS / 2);
-        const int rp = rot[P], rq = rot[Q];
-        if (!rp && !rq) continue;
-        const int i1 = pi[P], j1 = pj[P], i2 = pi[Q], j2 = pj[Q];
-        if (P == Q) {
-          const double aij = A[i1 * LS + j1];
-          const double t = tt[P];
-          A[i1 * LS + i1] -= t * aij;
-          A[j1 * LS + j1] += t * aij;
-          A[i1 * LS + j1] = 0.0;
-          A[j1 * LS + i1] = 0.0;
+      rotated |= r;
+      // A_next = R^T A R : this warp owns row pairs P = warp and warp + 16, column pair Q = lane
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int P = warp + 16 * h;
+        const int rp = __shfl_sync(0xffffffffu, r, P);
+        const double cp = __shfl_sync(0xffffffffu, c, P), sp = __shfl_sync(0xffffffffu, s, P);
+        const int i1 = __shfl_sync(0xffffffffu, a, P), j1 = __shfl_sync(0xffffffffu, b, P);
+        if (P == lane) {
+          const double x00 = Acur[i1 * LS + i1], x11 = Acur[j1 * LS + j1], x01 = Acur[i1 * LS + j1];
+          if (r) {
+            Anx[i1 * LS + i1] = x00 - t * x01;
+            Anx[j1 * LS + j1] = x11 + t * x01;
+            Anx[i1 * LS + j1] = 0.0;
+            Anx[j1 * LS + i1] = 0.0;
+          } else {
+            Anx[i1 * LS + i1] = x00;
+            Anx[j1 * LS + j1] = x11;
+            Anx[i1 * LS + j1] = x01;
+            Anx[j1 * LS + i1] = x01;
+          }
           continue;
         }
-        double b00 = A[i1 * LS + i2], b01 = A[i1 * LS + j2], b10 = A[j1 * LS + i2], b11 = A[j1 * LS + j2];
+        double b00 = Acur[i1 * LS + a], b01 = Acur[i1 * LS + b], b10 = Acur[j1 * LS + a], b11 = Acur[j1 * LS + b];
         if (rp) {
-          const double c = cs[P], s = sn[P];
-          const double n00 = c * b00 - s * b10, n01 = c * b01 - s * b11;
-          const double n10 = s * b00 + c * b10, n11 = s * b01 + c * b11;
+          const double n00 = cp * b00 - sp * b10, n01 = cp * b01 - sp * b11;
+          const double n10 = sp * b00 + cp * b10, n11 = sp * b01 + cp * b11;
           b00 = n00;
           b01 = n01;
           b10 = n10;
           b11 = n11;
         }
-        if (rq) {
-          const double c = cs[Q], s = sn[Q];
+        if (r) {
           const double n00 = c * b00 - s * b01, n01 = s * b00 + c * b01;
           const double n10 = c * b10 - s * b11, n11 = s * b10 + c * b11;
           b00 = n00;
@@ -250,44 +251,47 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
           b10 = n10;
           b11 = n11;
         }
-        A[i1 * LS + i2] = b00;
-        A[i1 * LS + j2] = b01;
-        A[j1 * LS + i2] = b10;
-        A[j1 * LS + j2] = b11;
+        Anx[i1 * LS + a] = b00;
+        Anx[i1 * LS + b] = b01;
+        Anx[j1 * LS + a] = b10;
+        Anx[j1 * LS + b] = b11;
       }
-      // W <- W R
-      for (int e = tid; e < PS * (PS / 2); e += LT) {
-        const int r = e / (PS / 2), Q = e % (PS / 2);
-        if (!rot[Q]) continue;
-        const int i2 = pi[Q], j2 = pj[Q];
-        const double c = cs[Q], s = sn[Q];
-        const double wi = Wl[i2 * LS + r], wj = Wl[j2 * LS + r];
-        Wl[i2 * LS + r] = c * wi - s * wj;
-        Wl[j2 * LS + r] = s * wi + c * wj;
+      // W <- W R on this warp's rows
+      if (r) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int row = warp + 16 * h;
+          const double wi = Wl[a * LS + row], wj = Wl[b * LS + row];
+          Wl[a * LS + row] = c * wi - s * wj;
+          Wl[b * LS + row] = s * wi + c * wj;
+        }
       }
+      __syncwarp();
+      double* tmp = Acur;
+      Acur = Anx;
+      Anx = tmp;
       __syncthreads();
     }
-    if (!any_rot) break;
+    if (!__syncthreads_or(rotated)) break;
   }
   // sorted Jacobi: order the local eigenvalues descending so large eigenvalues
   // migrate to the low blocks (the rank-of-diagonal permutation of W's columns)
-  __shared__ int sperm[PS];
   if (tid < PS) {
-    const double di = A[tid * LS + tid];
-    int r = 0;
+    const double di = Acur[tid * LS + tid];
+    int rk = 0;
     for (int j = 0; j < PS; ++j) {
-      const double dj = A[j * LS + j];
-      r += (dj > di) || (dj == di && j < tid);
+      const double dj = Acur[j * LS + j];
+      rk += (dj > di) || (dj == di && j < tid);
     }
-    sperm[r] = tid;
+    sperm[rk] = tid;
   }
   __syncthreads();
   // one Bjorck step on DMMA (warps 0-7), W column-major in Wl:
-  //   E = W^T W - I ;  W_new = W - W E / 2     (staged column-major in A's buffer)
-  double* E = Wl + PS * LS;
+  //   E = W^T W - I ;  W_new = W - W E / 2     (E in Anx, W_new staged in Acur)
+  double* E = Anx;
+  double* Wn = Acur;
   {
     double acc[2][4][2];
-    const int warp = tid >> 5;
     if (warp < 8) mm64<true, LS, LS>(Wl, Wl, acc);   // A(m,k) = Wl[m*LS+k] = W(k,m), B(k,n) = Wl[n*LS+k] = W(k,n)
     __syncthreads();
     if (warp < 8) store_acc<LS>(E, acc);
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     if (warp < 8) mm64<false, LS, LS>(Wl, E, acc);  // A(m,k) = Wl[k*LS+m] = W(m,k), B(k,n) = E(k,n)
     __syncthreads();
     if (warp < 8) {
-      const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+      const int g = lane >> 2, t4 = lane & 3;
       const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -305,15 +309,15 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e2 = 0; e2 < 2; ++e2) {
-            const int m = r0 + i * 8 + g, n = c0 + j * 8 + 2 * t + e2;
-            A[n * LS + m] = Wl[n * LS + m] - 0.5 * acc[i][j][e2];
+            const int m = r0 + i * 8 + g, n = c0 + j * 8 + 2 * t4 + e2;
+            Wn[n * LS + m] = Wl[n * LS + m] - 0.5 * acc[i][j][e2];
           }
     }
     __syncthreads();
   }
   for (int e = tid; e < PS * PS; e += LT) {
     const int j = e / PS, i = e % PS;
-    p.W[(int64_t)k * PS * PS + j * PS + i] = A[sperm[j] * LS + i];
+    p.W[(int64_t)k * PS * PS + j * PS + i] = Wn[sperm[j] * LS + i];
   }
   if (tid == 0) {
     p.flags[k] = 1;
@@ -345,14 +349,9 @@ __device__ __forceinline__ void load_slab(double* dst, const double* V, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
-  extern __shared__ double sm[];
-  double* X = sm;
-  double* WQ = X + PS * TS;
-  double* WP = WQ + PS * TS;
-  const int npairs = p.nb / 2;
-  const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
-  const int64_t b = blockIdx.x;
+// One task of the apply step (a G tile or a V slab); returns after its stores.
+__device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t ng, int npairs, double* X,
+                                           double* WQ, double* WP) {
   double acc[2][4][2];
   if (b < ng) {
     // G tile (P, Q), P <= Q: column-major enumeration of the upper triangle, b = Q(Q+1)/2 + P
@@ -423,6 +422,22 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   for (int e = threadIdx.x; e < PS * PS; e += AT) {
     const int j = e / PS, i = e % PS;
     p.V[local_index(qp, qq, j) * p.np + rc * PS + i] = X[j * TS + i];
+  }
+}
+
+// Persistent apply: a fixed grid (2 CTAs per SM) strides over all tasks; tasks of pairs
+// that needed no rotation cost two flag loads instead of a CTA launch.
+__global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
+  extern __shared__ double sm[];
+  double* X = sm;
+  double* WQ = X + PS * TS;
+  double* WP = WQ + PS * TS;
+  const int npairs = p.nb / 2;
+  const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
+  const int64_t ntasks = ng + (p.np / PS) * npairs;
+  for (int64_t b = blockIdx.x; b < ntasks; b += gridDim.x) {
+    apply_task(p, b, ng, npairs, X, WQ, WP);
+    __syncthreads();  // smem reuse by the next task
   }
 }
 
@@ -537,8 +552,8 @@ Layout layout(int64_t n) {
 size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
 
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, int max_sweeps, int* sweeps_out, double* flops_out, void* ws,
-             size_t ws_bytes, cudaStream_t st) {
+             double tol_rel, double tol_abs, double keep_floor, int max_sweeps, int* sweeps_out, double* flops_out,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace jac;
   HP_REQUIRE(n >= 0, "syev: negative order");
   if (sweeps_out) *sweeps_out = 0;
@@ -563,6 +578,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.nb = L.nb;
   p.tol_rel = tol_rel;
   p.tol_abs = tol_abs;
+  p.keep_floor = keep_floor;
   static const int local_sweeps = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 1;
   p.max_local_sweeps = local_sweeps;
 
@@ -582,6 +598,10 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
 
   const int npairs = L.nb / 2;
   const int64_t napply = (int64_t)npairs * (npairs + 1) / 2 + (L.np / PS) * npairs;
+  int nsm = 148, dev = 0;
+  HP_CHECK_CUDA(cudaGetDevice(&dev));
+  HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned apply_grid = (unsigned)std::min<int64_t>(napply, 2 * (int64_t)nsm);
   char* host_buf = nullptr;
   HP_CHECK_CUDA(cudaMallocHost(&host_buf, 32));
   HP_CHECK_CUDA(cudaMemsetAsync(p.mm_count, 0, 8, st));
@@ -597,7 +617,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     for (int r = 0; r < L.nb - 1; ++r) {
       p.round = r;
       jac_local<<<npairs, LT, local_smem, st>>>(p);
-      jac_apply<<<(unsigned)napply, AT, apply_smem, st>>>(p);
+      jac_apply<<<apply_grid, AT, apply_smem, st>>>(p);
       count_launches(2);
     }
     e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count

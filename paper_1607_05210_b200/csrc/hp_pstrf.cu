@@ -61,6 +61,46 @@ __device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
 
+// CTA-local argmax of the running diagonal over rows [r0, r1) -> partials[slot][blockIdx.x]
+__device__ __forceinline__ void local_argmax(const Params& p, int64_t r0, int64_t r1, int slot, double* sv, int* si) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int64_t i = r0 + tid; i < r1; i += PT) {
+    const double v = p.d[i];
+    if (better(v, (int)i, bv, bi)) {
+      bv = v;
+      bi = (int)i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    sv[warp] = bv;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double cv = sv[0];
+    int ci = si[0];
+    for (int w = 1; w < PT / 32; ++w)
+      if (better(sv[w], si[w], cv, ci)) {
+        cv = sv[w];
+        ci = si[w];
+      }
+    p.red_v[slot * 1024 + blockIdx.x] = cv;
+    p.red_i[slot * 1024 + blockIdx.x] = ci;
+  }
+}
+
+// One grid-wide barrier per column: the argmax partials for column j+1 are produced in the
+// same pass that computes column j (double-buffered by column parity).
 __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[PT / 32];
@@ -70,54 +110,20 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
   __shared__ double s_lp[PB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = gridDim.x;
-  // contiguous row slice of this CTA
   const int64_t per = (p.m + nblk - 1) / nblk;
   const int64_t r0 = blockIdx.x * per, r1 = min(p.m, r0 + per);
 
+  local_argmax(p, r0, r1, p.k0 & 1, sv, si);
+  grid.sync();
   for (int j = p.k0; j < p.k1; ++j) {
-    // ---- argmax of the running diagonal over unpivoted rows
-    double bv = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int64_t i = r0 + tid; i < r1; i += PT) {
-      const double v = p.d[i];
-      if (better(v, (int)i, bv, bi)) {
-        bv = v;
-        bi = (int)i;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (better(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      sv[warp] = bv;
-      si[warp] = bi;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double cv = sv[0];
-      int ci = si[0];
-      for (int w = 1; w < PT / 32; ++w)
-        if (better(sv[w], si[w], cv, ci)) {
-          cv = sv[w];
-          ci = si[w];
-        }
-      p.red_v[blockIdx.x] = cv;
-      p.red_i[blockIdx.x] = ci;
-    }
-    grid.sync();
-    // every CTA reduces the partials redundantly (identical result everywhere): warp 0,
-    // lane-strided loads + shuffle reduction (the partials live in L2)
+    const int slot = j & 1;
+    // every CTA reduces the partials redundantly (identical result everywhere)
     if (warp == 0) {
       double gv = -INFINITY;
       int gi = 0x7fffffff;
       for (int b = lane; b < (int)nblk; b += 32) {
-        const double v = __ldcg(p.red_v + b);
-        const int ii = __ldcg(p.red_i + b);
+        const double v = __ldcg(p.red_v + slot * 1024 + b);
+        const int ii = __ldcg(p.red_i + slot * 1024 + b);
         if (better(v, ii, gv, gi)) {
           gv = v;
           gi = ii;
@@ -143,15 +149,14 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
     // uniform across the grid (every CTA reduced the same partials); rank stays j.
     if (!(dp > p.tol)) return;
     const double ljj = sqrt(dp);
-    // L[p, t] for the panel columns so far (t in [k0, j))
-    for (int t = p.k0 + tid; t < j; t += PT) s_lp[t - p.k0] = p.L[(int64_t)t * p.ldl + pv];
+    for (int t = p.k0 + tid; t < j; t += PT) s_lp[t - p.k0] = __ldcg(p.L + (int64_t)t * p.ldl + pv);
     __syncthreads();
-    // ---- column j over the CTA's rows
     const double* acol = p.A + (int64_t)pv * p.lda;
     for (int64_t i = r0 + tid; i < r1; i += PT) {
       double li;
       if (i == pv) {
         li = ljj;
+        p.d[i] = -INFINITY;
       } else if (p.d[i] == -INFINITY) {
         li = 0.0;  // already pivoted: L is lower triangular in pivot order
       } else {
@@ -162,11 +167,10 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
       }
       p.L[(int64_t)j * p.ldl + i] = li;
     }
-    if (pv >= r0 && pv < r1 && tid == 0) {
-      p.d[pv] = -INFINITY;
-      p.piv[j] = pv;
-    }
+    if (tid == 0 && pv >= r0 && pv < r1) p.piv[j] = pv;
     if (blockIdx.x == 0 && tid == 0) *p.rank = j + 1;
+    __syncthreads();
+    local_argmax(p, r0, r1, slot ^ 1, sv, si);  // partials for column j+1
     grid.sync();
   }
 }
@@ -200,7 +204,7 @@ size_t pstrf_workspace_bytes(int64_t m) {
   const int64_t ld = (m + 1) & ~int64_t(1);
   size_t o = al((size_t)ld * m * 8);          // A
   o += al((size_t)m * 8);                       // d
-  o += al(2048 * 8) + al(2048 * 4) + al(64);    // partials + rank + scal
+  o += al(2048 * 8) + al(2048 * 4) + al(64);    // partials (2 x 1024) + rank + scal
   o += al(gemm_workspace_bytes(m, m, pc::PB, 1, 0));
   return o;
 }
@@ -247,7 +251,7 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pstrf_panel, PT, 0));
   const int rows_per_cta = 64;
   int grid = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), ceil_div(m, rows_per_cta));
-  grid = std::max(1, std::min(grid, 2048));
+  grid = std::max(1, std::min(grid, 1024));
 
   Params p{};
   p.A = A;
