@@ -144,6 +144,8 @@ int hp_transpose_rm_to_cm(const double* src, int64_t rows, int64_t cols, double*
 int hp_scale(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* row_mul, const double* row_div,
              const double* col_mul, double* dst, int64_t ldd, void* stream);
 int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, void* stream);
+/* C(i,i) += s for i < n (Bjorck / Newton-Schulz orthonormalisation of the Ritz basis). */
+int hp_add_diag(double* C, int64_t ldc, int64_t n, double s, void* stream);
 
 /* Deterministic sum of squares of a column-major block (residual energy of
  * actual_mean_error, hierarchy.py:237-253); out = device scalar. */

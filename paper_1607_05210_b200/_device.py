@@ -46,6 +46,8 @@ LAST_SPECTRUM: list = []
 POLISH_FACTOR = float(_os.environ.get("HP_EIG_POLISH_FACTOR", "1e-2"))
 POLISH_TOL_REL = float(_os.environ.get("HP_EIG_POLISH_TOL_REL", str(2.0 ** -52)))
 POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
+# absolute trigger of the preconditioned (H = L^T L) phase; the polish carries the final accuracy
+PC_TOL_ABS = float(_os.environ.get("HP_PC_TOL_ABS", str(16 * 2.0 ** -52)))
 
 
 class Profiler:
@@ -302,6 +304,48 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     return G, total, keep
 
 
+BJORCK_MAX_DRIFT = 0.05   # Newton-Schulz converges quadratically from here (3 steps to ~u)
+
+
+def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
+    """Make X orthonormal (any basis of its span).  Bjorck steps X <- X - X E / 2,
+    E = X^T X - I, while max|E| <= BJORCK_MAX_DRIFT (quadratic: drift -> ~drift^2); CholQR
+    (hp_reorthonormalize) otherwise.  Returns the initial drift."""
+    lib = N.load()
+    m, K = X.rows, X.cols
+    C = DevMat.empty(K, K)
+    drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
+    N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
+            "X^T X")
+    drift0 = drift = float(drift_dev.item())
+    ph.flops += float(m) * K * (K + 1)
+    if drift > BJORCK_MAX_DRIFT:
+        rws = _ws(lib.hp_reortho_workspace_bytes(m, K))
+        passes = ctypes.c_int(0)
+        N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, drift, ctypes.byref(passes),
+                                        rws.data_ptr(), rws.numel(), st), "orthonormalise X")
+        ph.flops += passes.value * 2.0 * m * K * K
+        return drift0
+    Y = DevMat.empty(m, K)
+    orig = X
+    for _ in range(6):
+        if drift <= 4 * 2.0 ** -52:
+            break
+        # C := X^T X - I (C holds X^T X); Y = X - X C / 2 ; X <- Y
+        N.check(lib.hp_add_diag(C.ptr, C.ld, K, -1.0, st), "C - I")
+        N.check(lib.hp_scale(X.ptr, X.ld, m, K, None, None, None, Y.ptr, Y.ld, st), "copy")
+        N.check(lib.hp_gemm(0, 1, m, K, K, X.vecset(), C.vecset(), -0.5, 1.0, Y.ptr, Y.ld, None, None, None, 0, 0,
+                            ws.data_ptr(), ws.numel(), st), "Bjorck step")
+        X, Y = Y, X
+        N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "X^T X")
+        drift = float(drift_dev.item())
+        ph.flops += 2.0 * m * K * K + float(m) * K * (K + 1)
+    if X is not orig:
+        N.check(lib.hp_scale(X.ptr, X.ld, m, K, None, None, None, orig.ptr, orig.ld, st), "copy back")
+    return drift0
+
+
 def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0):
     lib = N.load()
     lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
@@ -351,7 +395,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                 N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
                         "H = L^T L")
             del ws
-        lam, W, sweeps = _syev(H, r, st)
+        lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS if POLISH else None)
         nev = r
         basis, divide = Lf, True
         if POLISH and r:
@@ -369,31 +413,29 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                 # G2 = X^T G X then resolves the mixing inside the span.
                 ws = _ws(max(lib.hp_gemm_workspace_bytes(m, K, r, 0, 0), lib.hp_gemm_workspace_bytes(m, K, m, 0, 0),
                              lib.hp_gemm_workspace_bytes(K, K, m, 1, 0)))
-                with _phase("polish", 2.0 * m * r * K + 4.0 * m * m * K + 2.0 * m * K * K + float(m) * K * (K + 1)):
-                    Q0 = DevMat.empty(m, K)
+                Q0 = DevMat.empty(m, K)
+                with _phase("polish_q0", 2.0 * m * r * K):
                     N.check(lib.hp_gemm(0, 1, m, K, r, Lr.vecset(), W.vecset(), 1.0, 0.0, Q0.ptr, Q0.ld, None, None,
                                         sig_h.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "Q0 = L W / sigma")
-                    X = DevMat.empty(m, K)
+                X = DevMat.empty(m, K)
+                with _phase("polish_x", 2.0 * m * m * K):
                     N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), Q0.vecset(), 1.0, 0.0, X.ptr, X.ld, None, None,
                                         lam.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "X = G Q0 / lambda")
-                    del Q0
-                    C = DevMat.empty(K, K)
-                    drift_q = torch.zeros(1, dtype=torch.float64, device="cuda")
-                    N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_q.data_ptr(), ws.data_ptr(),
-                                         ws.numel(), st), "X^T X")
-                    rws = _ws(lib.hp_reortho_workspace_bytes(m, K))
-                    passes = ctypes.c_int(0)
-                    N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, float(drift_q.item()),
-                                                    ctypes.byref(passes), rws.data_ptr(), rws.numel(), st),
-                            "orthonormalise X")
-                    del rws, C
-                    T = DevMat.empty(m, K)
+                del Q0
+                ph = _phase("polish_orth", 0.0)
+                with ph:
+                    # any orthonormal basis of span(X) serves Rayleigh-Ritz: Bjorck / Newton-Schulz steps
+                    # X <- X (3 I - X^T X) / 2 (two DMMA GEMMs each, no sequential factorisation) while
+                    # the drift is small, CholQR otherwise
+                    drift_x = _orthonormalise_basis(X, ws, st, ph)
+                T = DevMat.empty(m, K)
+                G2 = DevMat.empty(K, K)
+                with _phase("polish_rr", 2.0 * m * m * K + float(m) * K * (K + 1)):
                     N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), X.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None,
                                         None, 0, 0, ws.data_ptr(), ws.numel(), st), "T = G X")
-                    G2 = DevMat.empty(K, K)
                     N.check(lib.hp_gemm(1, 1, K, K, m, X.vecset(), T.vecset(), 1.0, 0.0, G2.ptr, G2.ld, None, None,
                                         None, 1, 0, ws.data_ptr(), ws.numel(), st), "G2 = X^T G X")
-                    del T, ws
+                del T, ws
                 # G2 is nearly diagonal and graded: relative criterion, but never rotate two
                 # eigenvalues that are both below a tenth of the Gram cutoff (pod.py:284)
                 floor = 0.1 * float(cutoff) * lam_max_h * m

@@ -369,6 +369,13 @@ int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, in
   return pstrf_run(G, ldg, m, L, ldl, piv, tol_rel, rank, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int hp_add_diag(double* C, int64_t ldc, int64_t n, double s, void* stream) {
+  if (n <= 0) return HP_OK;
+  add_diag<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(C, ldc, n, s);
+  HP_CHECK_LAUNCH("add_diag");
+  return HP_OK;
+}
+
 size_t hp_sumsq_workspace_bytes(void) { return 1024 * sizeof(double); }
 
 int hp_sumsq(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, void* ws, size_t ws_bytes,

@@ -70,14 +70,16 @@ struct Params {
 };
 
 __device__ __forceinline__ void circle_pair(int nplayers, int r, int k, int& a, int& b) {
-  // round-robin "circle method": player nplayers-1 fixed, others rotate
+  // round-robin "circle method": player nplayers-1 fixed, others rotate (0 <= r, k < m)
   const int m = nplayers - 1;
   if (k == 0) {
     a = m;
-    b = r % m;
+    b = r;
   } else {
-    a = (r + k) % m;
-    b = (r - k + m) % m;
+    a = r + k;
+    if (a >= m) a -= m;
+    b = r - k + m;
+    if (b >= m) b -= m;
   }
 }
 
@@ -351,7 +353,7 @@ __device__ __forceinline__ void load_slab(double* dst, const double* V, int64_t 
 
 // One task of the apply step (a G tile or a V slab); returns after its stores.
 __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t ng, int npairs, double* X,
-                                           double* WQ, double* WP) {
+                                           double* WQ, double* WP, int& wq_loaded) {
   double acc[2][4][2];
   if (b < ng) {
     // G tile (P, Q), P <= Q: column-major enumeration of the upper triangle, b = Q(Q+1)/2 + P
@@ -365,7 +367,8 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
     block_pair(p, P, pp, pq);
     block_pair(p, Q, qp, qq);
     load_tile(X, p.G, p.np, pp, pq, qp, qq);
-    if (fQ) load_w(WQ, p.W + (int64_t)Q * PS * PS);
+    if (fQ && wq_loaded != Q) load_w(WQ, p.W + (int64_t)Q * PS * PS);
+    if (fQ) wq_loaded = Q;
     if (fP) load_w(WP, p.W + (int64_t)P * PS * PS);
     cp_async_commit();
     if (threadIdx.x == 0) atomicAdd(p.mm_count, (unsigned long long)(fP + fQ));
@@ -402,15 +405,17 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
     }
     return;
   }
-  // V slab: rows [rc*64, rc*64+64), columns of pair Q
+  // V slab: rows [rc*64, rc*64+64), columns of pair Q (Q-major, so consecutive tasks share W_Q)
   const int64_t vb = b - ng;
-  const int Q = (int)(vb % npairs);
-  const int64_t rc = vb / npairs;
+  const int64_t nrc = p.np / PS;
+  const int Q = (int)(vb / nrc);
+  const int64_t rc = vb % nrc;
   if (!p.flags[Q]) return;
   int qp, qq;
   block_pair(p, Q, qp, qq);
   load_slab(X, p.V, p.np, rc * PS, qp, qq);
-  load_w(WQ, p.W + (int64_t)Q * PS * PS);
+  if (wq_loaded != Q) load_w(WQ, p.W + (int64_t)Q * PS * PS);
+  wq_loaded = Q;
   cp_async_commit();
   if (threadIdx.x == 0) atomicAdd(p.mm_count, 1ull);
   cp_async_wait<0>();
@@ -425,8 +430,8 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
   }
 }
 
-// Persistent apply: a fixed grid (2 CTAs per SM) strides over all tasks; tasks of pairs
-// that needed no rotation cost two flag loads instead of a CTA launch.
+// Persistent apply: a fixed grid (2 CTAs per SM) walks all tasks; tasks of pairs that
+// needed no rotation cost two flag loads instead of a CTA launch.
 __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   extern __shared__ double sm[];
   double* X = sm;
@@ -435,8 +440,13 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   const int npairs = p.nb / 2;
   const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
   const int64_t ntasks = ng + (p.np / PS) * npairs;
-  for (int64_t b = blockIdx.x; b < ntasks; b += gridDim.x) {
-    apply_task(p, b, ng, npairs, X, WQ, WP);
+  // contiguous chunk per CTA: consecutive tasks mostly share the column pair Q, whose
+  // rotation then stays in shared memory
+  const int64_t chunk = (ntasks + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * chunk, b1 = min(ntasks, b0 + chunk);
+  int wq_loaded = -1;
+  for (int64_t b = b0; b < b1; ++b) {
+    apply_task(p, b, ng, npairs, X, WQ, WP, wq_loaded);
     __syncthreads();  // smem reuse by the next task
   }
 }
@@ -610,14 +620,20 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   double prev_off = INFINITY;
   unsigned long long mm_total = 0;
   const double floor_ratio = 512.0 * 2.220446049250313e-16;
-  static const bool trace = getenv("HP_JACOBI_TRACE") != nullptr;
+  static const int trace = getenv("HP_JACOBI_TRACE") ? atoi(getenv("HP_JACOBI_TRACE")) : 0;
+  cudaEvent_t ev[3];
+  if (trace > 1)
+    for (auto& e : ev) cudaEventCreate(&e);
   for (; sweep < max_sweeps; ++sweep) {
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
     if (e != cudaSuccess) break;
     for (int r = 0; r < L.nb - 1; ++r) {
       p.round = r;
+      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[0], st);
       jac_local<<<npairs, LT, local_smem, st>>>(p);
+      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[1], st);
       jac_apply<<<apply_grid, AT, apply_smem, st>>>(p);
+      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[2], st);
       count_launches(2);
     }
     e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
@@ -630,8 +646,15 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     const int worked = *reinterpret_cast<int*>(host_buf);
     const double off = *reinterpret_cast<double*>(host_buf + 16);
     mm_total = *reinterpret_cast<unsigned long long*>(host_buf + 24);
-    if (trace) fprintf(stderr, "[hp_syev n=%lld] sweep %d: pairs worked %d / %d, max off/diag %.3e\n", (long long)n,
-                       sweep, worked, npairs * (L.nb - 1), off);
+    if (trace) {
+      float t_local = 0.f, t_apply = 0.f;
+      if (trace > 1) {
+        cudaEventElapsedTime(&t_local, ev[0], ev[1]);
+        cudaEventElapsedTime(&t_apply, ev[1], ev[2]);
+      }
+      fprintf(stderr, "[hp_syev n=%lld] sweep %d: pairs worked %d / %d, max off/diag %.3e  (mid-round: local %.1f us, apply %.1f us)\n",
+              (long long)n, sweep, worked, npairs * (L.nb - 1), off, 1e3f * t_local, 1e3f * t_apply);
+    }
     if (worked == 0 || (off < floor_ratio && off > 0.5 * prev_off)) {
       status = HP_OK;
       break;
