@@ -67,6 +67,9 @@ struct Params {
   double tol_rel, tol_abs;
   double keep_floor;  // pairs whose diagonal entries are both below this never rotate
   int max_local_sweeps;
+  int* tile_mark;     // per G tile: stamp of the round whose "needed" pass already applied it
+  int stamp;
+  int phase;          // apply: 1 = tiles needed by the next round's local solves, 2 = the rest
 };
 
 __device__ __forceinline__ void circle_pair(int nplayers, int r, int k, int& a, int& b) {
@@ -88,6 +91,15 @@ __device__ __forceinline__ void block_pair(const Params& p, int k, int& bp, int&
   circle_pair(p.nb, p.round, k, a, b);
   bp = min(a, b);
   bq = max(a, b);
+}
+
+// index k of the pair that contains block x in round r (inverse of circle_pair)
+__device__ __forceinline__ int pair_of(int nb, int r, int x) {
+  const int m = nb - 1;
+  if (x == m || x == r) return 0;
+  int k = x - r;
+  if (k < 0) k += m;
+  return k <= (m - 1) / 2 ? k : m - k;
 }
 
 __device__ __forceinline__ int64_t local_index(int bp, int bq, int i) {
@@ -361,6 +373,7 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
     while ((int64_t)(Q + 1) * (Q + 2) / 2 <= b) ++Q;
     while ((int64_t)Q * (Q + 1) / 2 > b) --Q;
     const int P = (int)(b - (int64_t)Q * (Q + 1) / 2);
+    if (p.phase == 2 && p.tile_mark[b] == p.stamp) return;  // applied by the "needed" pass
     const int fP = p.flags[P], fQ = p.flags[Q];
     if (!fP && !fQ) return;
     int pp, pq, qp, qq;
@@ -439,6 +452,31 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   double* WP = WQ + PS * TS;
   const int npairs = p.nb / 2;
   const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
+  if (p.phase == 1) {
+    // the tiles the next round's local solves read: every pair's diagonal tile and, for each
+    // pair (x, y) of round r+1, the tile holding block (x, y); claimed with the round stamp
+    __shared__ int go;
+    const int rn = (p.round + 1) % (p.nb - 1);
+    int wq_loaded = -1;
+    for (int t = blockIdx.x; t < 2 * npairs; t += gridDim.x) {
+      int P, Q;
+      if (t < npairs) {
+        P = Q = t;
+      } else {
+        int x, y;
+        circle_pair(p.nb, rn, t - npairs, x, y);
+        const int P1 = pair_of(p.nb, p.round, x), P2 = pair_of(p.nb, p.round, y);
+        P = min(P1, P2);
+        Q = max(P1, P2);
+      }
+      const int64_t b = (int64_t)Q * (Q + 1) / 2 + P;
+      if (threadIdx.x == 0) go = atomicExch(p.tile_mark + b, p.stamp) != p.stamp;
+      __syncthreads();
+      if (go) apply_task(p, b, ng, npairs, X, WQ, WP, wq_loaded);
+      __syncthreads();
+    }
+    return;
+  }
   const int64_t ntasks = ng + (p.np / PS) * npairs;
   // contiguous chunk per CTA: consecutive tasks mostly share the column pair Q, whose
   // rotation then stays in shared memory
@@ -523,7 +561,7 @@ __global__ void gather_vectors(const double* Vp, int64_t np, int64_t n, const in
 struct Layout {
   int64_t np;
   int nb;
-  size_t off_G, off_V, off_W, off_flags, off_counter, off_scal, off_perm, off_rq, off_gemm, total;
+  size_t off_G, off_V, off_W, off_flags, off_marks, off_counter, off_scal, off_perm, off_rq, off_gemm, total;
 };
 
 Layout layout(int64_t n) {
@@ -540,9 +578,11 @@ Layout layout(int64_t n) {
   L.off_V = o;
   o = al(o + (size_t)L.np * L.np * 8);
   L.off_W = o;
-  o = al(o + (size_t)(nb / 2) * PS * PS * 8);
+  o = al(o + 2 * (size_t)(nb / 2) * PS * PS * 8);  // double-buffered by round parity
   L.off_flags = o;
-  o = al(o + (size_t)(nb / 2) * 4);
+  o = al(o + 2 * (size_t)(nb / 2) * 4);
+  L.off_marks = o;
+  o = al(o + (size_t)(nb / 2) * (nb / 2 + 1) / 2 * 4);
   L.off_counter = o;
   o = al(o + 64);
   L.off_scal = o;
@@ -576,8 +616,11 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   Params p{};
   p.G = reinterpret_cast<double*>(base + L.off_G);
   p.V = reinterpret_cast<double*>(base + L.off_V);
-  p.W = reinterpret_cast<double*>(base + L.off_W);
-  p.flags = reinterpret_cast<int*>(base + L.off_flags);
+  double* W_base = reinterpret_cast<double*>(base + L.off_W);
+  int* flags_base = reinterpret_cast<int*>(base + L.off_flags);
+  p.W = W_base;
+  p.flags = flags_base;
+  p.tile_mark = reinterpret_cast<int*>(base + L.off_marks);
   p.counter = reinterpret_cast<int*>(base + L.off_counter);
   p.maxoff = reinterpret_cast<double*>(base + L.off_counter + 16);
   p.mm_count = reinterpret_cast<unsigned long long*>(base + L.off_counter + 24);
@@ -611,7 +654,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   int nsm = 148, dev = 0;
   HP_CHECK_CUDA(cudaGetDevice(&dev));
   HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned apply_grid = (unsigned)std::min<int64_t>(napply, 2 * (int64_t)nsm);
+
   char* host_buf = nullptr;
   HP_CHECK_CUDA(cudaMallocHost(&host_buf, 32));
   HP_CHECK_CUDA(cudaMemsetAsync(p.mm_count, 0, 8, st));
@@ -624,22 +667,47 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   cudaEvent_t ev[3];
   if (trace > 1)
     for (auto& e : ev) cudaEventCreate(&e);
+  // Two streams: round r+1's local solves (stream st2) overlap round r's "rest" apply pass
+  // (stream st); they only need the tiles of round r's "needed" pass.
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t e_needed = nullptr, e_local = nullptr;
+  HP_CHECK_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  HP_CHECK_CUDA(cudaEventCreateWithFlags(&e_needed, cudaEventDisableTiming));
+  HP_CHECK_CUDA(cudaEventCreateWithFlags(&e_local, cudaEventDisableTiming));
+  HP_CHECK_CUDA(cudaMemsetAsync(p.tile_mark, 0, (size_t)npairs * (npairs + 1) / 2 * 4, st));
+  const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, nsm);
+  const unsigned rest_grid = (unsigned)std::min<int64_t>(napply, 2 * (int64_t)nsm);
+  int stamp = 0;
   for (; sweep < max_sweeps; ++sweep) {
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
     if (e != cudaSuccess) break;
+    cudaEventRecord(e_needed, st);
     for (int r = 0; r < L.nb - 1; ++r) {
       p.round = r;
-      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[0], st);
-      jac_local<<<npairs, LT, local_smem, st>>>(p);
-      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[1], st);
-      jac_apply<<<apply_grid, AT, apply_smem, st>>>(p);
+      p.W = W_base + (size_t)(r & 1) * npairs * PS * PS;
+      p.flags = flags_base + (size_t)(r & 1) * npairs;
+      p.stamp = ++stamp;
+      cudaStreamWaitEvent(st2, e_needed, 0);
+      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[0], st2);
+      jac_local<<<npairs, LT, local_smem, st2>>>(p);
+      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[1], st2);
+      cudaEventRecord(e_local, st2);
+      cudaStreamWaitEvent(st, e_local, 0);
+      p.phase = 1;
+      jac_apply<<<needed_grid, AT, apply_smem, st>>>(p);
+      cudaEventRecord(e_needed, st);
+      p.phase = 2;
+      jac_apply<<<rest_grid, AT, apply_smem, st>>>(p);
       if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[2], st);
-      count_launches(2);
+      count_launches(3);
     }
     e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       cudaFreeHost(host_buf);
+      cudaEventDestroy(e_needed);
+      cudaEventDestroy(e_local);
+      cudaStreamDestroy(st2);
       set_error(std::string("syev sweep: ") + cudaGetErrorString(e));
       return HP_ECUDA;
     }
@@ -662,6 +730,9 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     prev_off = off;
   }
   cudaFreeHost(host_buf);
+  cudaEventDestroy(e_needed);
+  cudaEventDestroy(e_local);
+  cudaStreamDestroy(st2);
   if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
   // algorithmic flops of the DMMA rotation products (+ the Rayleigh-quotient GEMM below)
   if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + 2.0 * (double)n * n * (double)L.np;
