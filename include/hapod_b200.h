@@ -96,14 +96,15 @@ int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, in
  * first nvec eigenvectors in V.  Replaces scipy.linalg.eigh + reversal
  * (pod.py:329-331, 386-388).  Parallel two-sided block Jacobi; synchronises
  * the stream once per sweep.  Returns HP_ELINALG if max_sweeps is reached.
- * A pair (i,j) is rotated iff |g_ij| > tol_abs*max|g_ii|, |g_ij| > tol_rel*sqrt|g_ii g_jj|
- * and max(g_ii, g_jj) >= keep_floor (mixing among eigenvalues that are all below the
+ * A pair (i,j) is rotated iff |g_ij| > tol_abs*max|g_ii|, |g_ij| > tol_rel*sqrt|g_ii g_jj|,
+ * |g_ij| > tol_angle*|g_jj - g_ii| (the rotation angle is not negligible) and
+ * max(g_ii, g_jj) >= keep_floor (mixing among eigenvalues that are all below the
  * floor never reaches the output).  sweeps / flops (nullable, host) receive the sweep
  * count and the algorithmic flops of its DMMA products. */
 size_t hp_syev_workspace_bytes(int64_t n);
 int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-            double tol_rel, double tol_abs, double keep_floor, int max_sweeps, int* sweeps, double* flops, void* ws,
-            size_t ws_bytes, void* stream);
+            double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
+            double* flops, void* ws, size_t ws_bytes, void* stream);
 
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
  * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank

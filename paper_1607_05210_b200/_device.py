@@ -46,6 +46,8 @@ LAST_SPECTRUM: list = []
 POLISH_FACTOR = float(_os.environ.get("HP_EIG_POLISH_FACTOR", "1e-2"))
 POLISH_TOL_REL = float(_os.environ.get("HP_EIG_POLISH_TOL_REL", str(2.0 ** -52)))
 POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
+# rotations whose angle |g_ij| / |g_jj - g_ii| is below this change no output digit
+POLISH_TOL_ANGLE = float(_os.environ.get("HP_EIG_POLISH_TOL_ANGLE", "1e-14"))
 # absolute trigger of the preconditioned (H = L^T L) phase; the polish carries the final accuracy
 PC_TOL_ABS = float(_os.environ.get("HP_PC_TOL_ABS", str(16 * 2.0 ** -52)))
 
@@ -346,7 +348,7 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
     return drift0
 
 
-def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0):
+def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0, tol_angle=0.0):
     lib = N.load()
     lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
     V = DevMat.empty(n, n)
@@ -357,7 +359,7 @@ def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, 
     with ph:
         N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n,
                             JACOBI_TOL_REL if tol_rel is None else tol_rel,
-                            JACOBI_TOL_ABS if tol_abs is None else tol_abs, float(keep_floor),
+                            JACOBI_TOL_ABS if tol_abs is None else tol_abs, float(tol_angle), float(keep_floor),
                             JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
                             ws.numel(), st), "eigensolve")
         ph.flops = eflops.value
@@ -440,7 +442,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                 # eigenvalues that are both below a tenth of the Gram cutoff (pod.py:284)
                 floor = 0.1 * float(cutoff) * lam_max_h * m
                 lam, W, sweeps2 = _syev(G2, K, st, "eigensolve_polish", tol_rel=POLISH_TOL_REL,
-                                        tol_abs=POLISH_TOL_ABS, keep_floor=floor)
+                                        tol_abs=POLISH_TOL_ABS, keep_floor=floor, tol_angle=POLISH_TOL_ANGLE)
                 sweeps += sweeps2
                 nev = K
                 basis, divide = X, False

@@ -66,6 +66,7 @@ struct Params {
   const double* scal; // scal[0] = max |g_ii| of the input
   double tol_rel, tol_abs;
   double keep_floor;  // pairs whose diagonal entries are both below this never rotate
+  double tol_angle;   // pairs whose rotation angle |g_ij| / |g_jj - g_ii| is below this never rotate
   int max_local_sweeps;
   int* tile_mark;     // per G tile: stamp of the round whose "needed" pass already applied it
   int stamp;
@@ -107,9 +108,10 @@ __device__ __forceinline__ int64_t local_index(int bp, int bq, int i) {
 }
 
 __device__ __forceinline__ bool needs_rotation(double aij, double aii, double ajj, double tr, double ta,
-                                               double floor_ = 0.0) {
+                                               double floor_ = 0.0, double tang = 0.0) {
   const double a = fabs(aij);
-  return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj)) && (floor_ <= 0.0 || fmax(aii, ajj) >= floor_);
+  return a > ta && a > tr * sqrt(fabs(aii) * fabs(ajj)) && (floor_ <= 0.0 || fmax(aii, ajj) >= floor_) &&
+         a > tang * fabs(ajj - aii);
 }
 
 // C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     if (i < j) {
       const double aij = Acur[i * LS + j];
       moff = fmax(moff, fabs(aij));
-      if (needs_rotation(aij, Acur[i * LS + i], Acur[j * LS + j], tr, ta, p.keep_floor)) mine = 1;
+      if (needs_rotation(aij, Acur[i * LS + i], Acur[j * LS + j], tr, ta, p.keep_floor, p.tol_angle)) mine = 1;
     }
   }
   {
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
       int a, b;
       circle_pair(PS, step, lane, a, b);
       const double aii = Acur[a * LS + a], ajj = Acur[b * LS + b], aij = Acur[a * LS + b];
-      const int r = needs_rotation(aij, aii, ajj, tr, tloc, p.keep_floor);
+      const int r = needs_rotation(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
       double c = 1.0, s = 0.0, t = 0.0;
       if (r) {
         const double theta = (ajj - aii) / (2.0 * aij);
@@ -602,8 +604,8 @@ Layout layout(int64_t n) {
 size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
 
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, double keep_floor, int max_sweeps, int* sweeps_out, double* flops_out,
-             void* ws, size_t ws_bytes, cudaStream_t st) {
+             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps_out,
+             double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace jac;
   HP_REQUIRE(n >= 0, "syev: negative order");
   if (sweeps_out) *sweeps_out = 0;
@@ -632,6 +634,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.tol_rel = tol_rel;
   p.tol_abs = tol_abs;
   p.keep_floor = keep_floor;
+  p.tol_angle = tol_angle;
   static const int local_sweeps = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 1;
   p.max_local_sweeps = local_sweeps;
 

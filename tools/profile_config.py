@@ -44,6 +44,7 @@ def main():
         t0 = time.perf_counter()
         if a.workers > 1:
             res, stats = H.run_parallel(tree, leaves, tol, worker_count=a.workers)
+            print("   wave times (s):", [round(w, 3) for w in stats.wave_times])
         else:
             res = H.run_hapod(tree, leaves, tol)
         torch.cuda.synchronize()
