@@ -11,7 +11,7 @@ snapshot set (16 leaf PODs + the root POD, every kernel of the hot path).
 value  : whole-job snapshot columns per second with S resident in HBM.
 e2e    : the same through the public API from pinned HOST memory: each step
          SnapshotBlock(space, host S) (H2D copy + device finiteness check),
-         distribute_columns, assign_tolerances, run_hapod, sigmas read back.
+         distribute_columns, assign_tolerances, run_parallel, sigmas read back.
 roofline: the dominant kernel family by device time inside the timed region
          (CUDA events on the launching stream), its algorithmic FP64 flops
           / its time, against the measured FP64 DMMA peak.

@@ -173,11 +173,25 @@ class DevMat:
         return out
 
 
-def upload(values, check_finite: bool = True) -> DevMat:
+_COPY_STREAM = None
+
+
+def copy_stream():
+    """One shared host-to-device copy stream: deferred uploads issued by pooled workers
+    serialise on it in request order, so the first leaf computes while the next arrive."""
+    global _COPY_STREAM
+    if _COPY_STREAM is None:
+        _COPY_STREAM = torch.cuda.Stream()
+    return _COPY_STREAM
+
+
+def upload(values, check_finite: bool = True, via=None) -> DevMat:
     """Host (numpy / torch CPU) or device (torch CUDA) d x m array -> DevMat.
 
     F-contiguous inputs are copied straight into the column-major layout;
-    C-contiguous ones are staged and transposed on the device."""
+    C-contiguous ones are staged and transposed on the device.  ``via``: a copy
+    stream for the host-to-device transfer of column-major host inputs (the
+    current stream waits on it)."""
     require_cuda()
     lib = N.load()
     if torch.is_tensor(values):
@@ -193,10 +207,17 @@ def upload(values, check_finite: bool = True) -> DevMat:
     d, m = int(t.shape[0]), int(t.shape[1])
     out = DevMat.empty(d, m)
     if d and m:
-        if t.stride(0) == 1 and t.stride(1) == d:            # column-major source
-            src = t.as_strided((m, d), (d, 1))
+        if t.stride(0) == 1 and t.stride(1) >= d:            # column-major source (possibly a column view)
+            src = t.as_strided((m, d), (t.stride(1), 1))
             dst = out.storage[: out.ld * m].view(m, out.ld)[:, :d]
-            dst.copy_(src, non_blocking=True)
+            if via is not None and not t.is_cuda:
+                cur = torch.cuda.current_stream()
+                via.wait_stream(cur)  # the destination was allocated on the current stream
+                with torch.cuda.stream(via):
+                    dst.copy_(src, non_blocking=True)
+                cur.wait_stream(via)
+            else:
+                dst.copy_(src, non_blocking=True)
         else:                                                  # row-major (or strided) source
             tc = t.contiguous() if not (t.is_cuda and t.is_contiguous()) else t
             dev = tc.to("cuda", non_blocking=True) if not tc.is_cuda else tc

@@ -114,13 +114,20 @@ class SnapshotBlock:
     """A d x m column block of snapshots living in one space (pod.py:100-121).
 
     ``values`` may be a NumPy array (any order), a CPU or a CUDA torch tensor.
-    The block is uploaded to HBM (column-major) and checked for non-finite
-    entries on the device at construction, as the reference does on the host
-    (pod.py:115-116)."""
+    By default the block is uploaded to HBM (column-major) and checked for
+    non-finite entries on the device at construction, as the reference does on
+    the host (pod.py:115-116).
+
+    ``defer_upload=True`` (host inputs only) keeps the host buffer and uploads
+    on first device use, on the caller's current CUDA stream; column views
+    (``column_block``, ``distribute_columns``) upload only their own columns.
+    Under ``run_parallel`` every leaf's host-to-device copy then overlaps the
+    other leaves' PODs.  The finiteness check (ValueError) happens at that
+    first use instead of at construction."""
 
     __slots__ = ("space", "_dev", "_host", "_count")
 
-    def __init__(self, space: InnerProductSpace, values):
+    def __init__(self, space: InnerProductSpace, values, defer_upload: bool = False):
         if _is_tensor(values):
             shape = tuple(values.shape)
         else:
@@ -132,6 +139,11 @@ class SnapshotBlock:
             raise ValueError(f"snapshot rows {shape[0]} do not match space dimension {space.dimension}")
         object.__setattr__(self, "space", space)
         object.__setattr__(self, "_count", int(shape[1]))
+        is_device = _is_tensor(values) and values.is_cuda
+        if defer_upload and not is_device:
+            object.__setattr__(self, "_host", values)
+            object.__setattr__(self, "_dev", None)
+            return
         object.__setattr__(self, "_host", None if _is_tensor(values) else values)
         object.__setattr__(self, "_dev", D.upload(values))
 
@@ -153,6 +165,8 @@ class SnapshotBlock:
 
     @property
     def device(self) -> "D.DevMat":
+        if self._dev is None:  # deferred upload: now, through the shared copy stream
+            object.__setattr__(self, "_dev", D.upload(self._host, via=D.copy_stream()))
         return self._dev
 
     @property
@@ -160,13 +174,22 @@ class SnapshotBlock:
         if self._host is None:
             object.__setattr__(self, "_host", self._dev.to_numpy())
         v = self._host
+        if _is_tensor(v):
+            v = v.numpy()
         if isinstance(v, np.ndarray) and v.flags.writeable:
             v = v.view()
             v.setflags(write=False)
         return v
 
     def column_block(self, j0: int, j1: int) -> "SnapshotBlock":
-        """Columns j0:j1 as a new block sharing device storage (no copy)."""
+        """Columns j0:j1 as a new block sharing storage (device view, or a deferred host view)."""
+        if self._dev is None:
+            obj = SnapshotBlock.__new__(SnapshotBlock)
+            object.__setattr__(obj, "space", self.space)
+            object.__setattr__(obj, "_count", j1 - j0)
+            object.__setattr__(obj, "_host", self._host[:, j0:j1])
+            object.__setattr__(obj, "_dev", None)
+            return obj
         host = None
         if isinstance(self._host, np.ndarray):
             host = self._host[:, j0:j1]

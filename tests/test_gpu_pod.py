@@ -292,3 +292,22 @@ def test_gramian_public():
     ref = vals.T @ (w[:, None] * vals)
     assert np.max(np.abs(g - ref)) < 1e-12
     assert np.array_equal(g, g.T)
+
+
+def test_deferred_upload_matches_eager_and_checks_finiteness():
+    vals = O.synthetic_decay(500, 256, 0.05, seed=3)
+    sp = euclid(500)
+    host = torch.from_numpy(np.asfortranarray(vals).T.copy()).pin_memory().t()  # column-major pinned
+    tree = H.build_star(4)
+    eager = H.distribute_columns(tree, H.SnapshotBlock(sp, vals))
+    lazy = H.distribute_columns(tree, H.SnapshotBlock(sp, host, defer_upload=True))
+    tol = H.assign_tolerances(tree, eager, 1e-3, omega=0.75)
+    a = H.run_hapod(tree, eager, tol)
+    b, _ = H.run_parallel(tree, lazy, tol, worker_count=4)
+    assert np.array_equal(a.modes.sigmas, b.modes.sigmas)
+    assert np.array_equal(a.modes.modes, b.modes.modes)
+    bad = np.array(vals)
+    bad[3, 7] = np.inf
+    blk = H.SnapshotBlock(sp, bad, defer_upload=True)  # no check yet
+    with pytest.raises(ValueError):
+        H.pod(blk, 0.1)
