@@ -83,14 +83,15 @@ int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F
 
 /* K2a -- eigensolver preconditioner: pivoted Cholesky G = L L^T + E with
  * complete diagonal pivoting, L (m x r) with rows in the ORIGINAL order, until
- * the largest remaining pivot <= tol_rel * max|G_ii| (E = rounding noise).
+ * the largest remaining pivot <= max(tol_rel * max|G_ii|, tol_lam * lam_est), lam_est a
+ * power-iteration lower bound of lambda_max (8 GEMVs; skipped when tol_lam = 0).
  * The eigenvalues of G are those of H = L^T L; its eigenvectors
  * V = L W Lambda^{-1/2} (W = eigenvectors of H).  piv (device, m ints)
  * receives the pivot order; rank (host) receives r.  Synchronises once per
  * 128-column panel. */
 size_t hp_pstrf_workspace_bytes(int64_t m);
 int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
-             int64_t* rank, void* ws, size_t ws_bytes, void* stream);
+             double tol_lam, int64_t* rank, void* ws, size_t ws_bytes, void* stream);
 
 /* K2 -- all eigenpairs of the symmetric n x n G, eigenvalues descending,
  * first nvec eigenvectors in V.  Replaces scipy.linalg.eigh + reversal
@@ -99,12 +100,14 @@ int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, in
  * A pair (i,j) is rotated iff |g_ij| > tol_abs*max|g_ii|, |g_ij| > tol_rel*sqrt|g_ii g_jj|,
  * |g_ij| > tol_angle*|g_jj - g_ii| (the rotation angle is not negligible) and
  * max(g_ii, g_jj) >= keep_floor (mixing among eigenvalues that are all below the
- * floor never reaches the output).  sweeps / flops (nullable, host) receive the sweep
- * count and the algorithmic flops of its DMMA products. */
+ * floor never reaches the output).  refine != 0: eigenvalues are Rayleigh quotients
+ * v^T G v / v^T v against the input (one extra n^3 GEMM), else the converged diagonal.
+ * sweeps / flops (nullable, host) receive the sweep count and the algorithmic flops of
+ * its DMMA products. */
 size_t hp_syev_workspace_bytes(int64_t n);
 int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-            double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
-            double* flops, void* ws, size_t ws_bytes, void* stream);
+            double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
+            int* sweeps, double* flops, void* ws, size_t ws_bytes, void* stream);
 
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
  * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank

@@ -44,6 +44,7 @@ POLISH = _os.environ.get("HP_EIG_POLISH", "1") != "0"
 KEEP_SPECTRUM = False   # diagnostics: keep the last node's eigenvalues in LAST_SPECTRUM
 LAST_SPECTRUM: list = []
 POLISH_FACTOR = float(_os.environ.get("HP_EIG_POLISH_FACTOR", "1e-2"))
+PSTRF_POLISH_MARGIN = float(_os.environ.get("HP_PSTRF_POLISH_MARGIN", "0.25"))
 POLISH_TOL_REL = float(_os.environ.get("HP_EIG_POLISH_TOL_REL", str(2.0 ** -52)))
 POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
 # rotations whose angle |g_ij| / |g_jj - g_ii| is below this change no output digit
@@ -369,7 +370,8 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
     return drift0
 
 
-def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0, tol_angle=0.0):
+def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0, tol_angle=0.0,
+          refine=True):
     lib = N.load()
     lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
     V = DevMat.empty(n, n)
@@ -381,7 +383,7 @@ def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, 
         N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n,
                             JACOBI_TOL_REL if tol_rel is None else tol_rel,
                             JACOBI_TOL_ABS if tol_abs is None else tol_abs, float(tol_angle), float(keep_floor),
-                            JACOBI_MAX_SWEEPS, ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
+                            JACOBI_MAX_SWEEPS, int(refine), ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
                             ws.numel(), st), "eigensolve")
         ph.flops = eflops.value
     return lam, V, sweeps.value
@@ -406,8 +408,11 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         rank = ctypes.c_int64(0)
         ws = _ws(lib.hp_pstrf_workspace_bytes(m))
         with _phase("pstrf", float(m) ** 3 / 3.0):
-            N.check(lib.hp_pstrf(G.ptr, G.ld, m, Lf.ptr, Lf.ld, piv.data_ptr(), PSTRF_TOL, ctypes.byref(rank),
-                                 ws.data_ptr(), ws.numel(), st), "pivoted Cholesky")
+            # with the polish, pivots below a quarter of its floor (lambda <= POLISH_FACTOR * cutoff
+            # * lambda_max * m) only feed directions the subspace step damps anyway
+            tol_lam = PSTRF_POLISH_MARGIN * POLISH_FACTOR * float(cutoff) * m if POLISH else 0.0
+            N.check(lib.hp_pstrf(G.ptr, G.ld, m, Lf.ptr, Lf.ld, piv.data_ptr(), PSTRF_TOL, tol_lam,
+                                 ctypes.byref(rank), ws.data_ptr(), ws.numel(), st), "pivoted Cholesky")
         del ws
         r = int(rank.value)
         Lr = Lf.view_cols(0, r)
@@ -418,7 +423,8 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                 N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
                         "H = L^T L")
             del ws
-        lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS if POLISH else None)
+        # with the polish, H's eigenvalues only select K and scale Q0: no Rayleigh refinement
+        lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS if POLISH else None, refine=not POLISH)
         nev = r
         basis, divide = Lf, True
         if POLISH and r:

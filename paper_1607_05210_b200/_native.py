@@ -42,9 +42,10 @@ _SIGNATURES = {
     "hp_block_gram_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "hp_block_gram": (c_int, [VecSet, c_vp, c_i64, VecSet, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_size, c_vp]),
     "hp_pstrf_workspace_bytes": (c_size, [c_i64]),
-    "hp_pstrf": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_dbl, ctypes.POINTER(c_i64), c_vp, c_size, c_vp]),
+    "hp_pstrf": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_dbl, c_dbl, ctypes.POINTER(c_i64), c_vp, c_size,
+                         c_vp]),
     "hp_syev_workspace_bytes": (c_size, [c_i64]),
-    "hp_syev": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int,
+    "hp_syev": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_int,
                         ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), c_vp, c_size, c_vp]),
     "hp_truncate": (c_int, [c_vp, c_i64, c_dbl, c_dbl, c_i64, c_vp, c_vp, c_vp]),
     "hp_assemble_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),

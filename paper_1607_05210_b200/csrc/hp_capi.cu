@@ -29,8 +29,8 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
 size_t syev_workspace_bytes(int64_t n);
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps_out,
-             double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st);
+             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
+             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st);
 int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
                  cudaStream_t st);
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
@@ -47,7 +47,7 @@ int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* 
               cudaStream_t st);
 size_t pstrf_workspace_bytes(int64_t m);
 int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
-              int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st);
+              double tol_lam, int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st);
 
 static inline VecSet vs(const hp_vecset& v) { return VecSet{v.base, v.ld, v.table}; }
 
@@ -214,10 +214,10 @@ int hp_block_gram(hp_vecset Phi, const double* sigma, int64_t n_old, hp_vecset F
 size_t hp_syev_workspace_bytes(int64_t n) { return syev_workspace_bytes(n); }
 
 int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-            double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
-            double* flops, void* ws, size_t ws_bytes, void* stream) {
-  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, tol_angle, keep_floor, max_sweeps, sweeps,
-                  flops, ws, ws_bytes, (cudaStream_t)stream);
+            double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
+            int* sweeps, double* flops, void* ws, size_t ws_bytes, void* stream) {
+  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, tol_angle, keep_floor, max_sweeps, refine,
+                  sweeps, flops, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int hp_truncate(const double* lam_desc, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info4,
@@ -364,9 +364,9 @@ int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, 
 size_t hp_pstrf_workspace_bytes(int64_t m) { return pstrf_workspace_bytes(m); }
 
 int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
-             int64_t* rank, void* ws, size_t ws_bytes, void* stream) {
+             double tol_lam, int64_t* rank, void* ws, size_t ws_bytes, void* stream) {
   HP_REQUIRE(m >= 0 && ldg >= m && ldl >= m, "hp_pstrf: bad dimensions");
-  return pstrf_run(G, ldg, m, L, ldl, piv, tol_rel, rank, ws, ws_bytes, (cudaStream_t)stream);
+  return pstrf_run(G, ldg, m, L, ldl, piv, tol_rel, tol_lam, rank, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int hp_add_diag(double* C, int64_t ldc, int64_t n, double s, void* stream) {

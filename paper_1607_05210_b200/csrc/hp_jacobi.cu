@@ -517,15 +517,16 @@ __global__ void max_abs_diag(const double* Gp, int64_t np, int64_t n, double* ou
 // eigenvalue drift that the accumulated local rotations leave in diag(G).
 // Columns whose real part (rows < n) vanishes are padding eigenvectors (exact
 // unit vectors of the zero padding, never mixed with real coordinates): -inf.
+// Y == nullptr: no refinement, the value is the converged diagonal entry Y0[col*ldy0 + col].
 __global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t ldy, int64_t n, int64_t ncols,
-                        double* out) {
+                        double* out, const double* diag_src = nullptr, int64_t ld_diag = 0) {
   const int64_t col = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (col >= ncols) return;
   double s = 0.0, nn = 0.0;
   for (int64_t k = lane; k < n; k += 32) {
     const double v = V[col * ldv + k];
-    s += v * Y[col * ldy + k];
+    if (Y) s += v * Y[col * ldy + k];
     nn += v * v;
   }
 #pragma unroll
@@ -533,7 +534,7 @@ __global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t l
     s += __shfl_xor_sync(0xffffffffu, s, o);
     nn += __shfl_xor_sync(0xffffffffu, nn, o);
   }
-  if (lane == 0) out[col] = nn > 0.5 ? s / nn : -INFINITY;
+  if (lane == 0) out[col] = nn > 0.5 ? (Y ? s / nn : diag_src[col * ld_diag + col]) : -INFINITY;
 }
 
 // rank of each value in descending order, ties broken by index
@@ -604,8 +605,8 @@ Layout layout(int64_t n) {
 size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
 
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
-             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps_out,
-             double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
+             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace jac;
   HP_REQUIRE(n >= 0, "syev: negative order");
   if (sweeps_out) *sweeps_out = 0;
@@ -738,21 +739,26 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   cudaStreamDestroy(st2);
   if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
   // algorithmic flops of the DMMA rotation products (+ the Rayleigh-quotient GEMM below)
-  if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + 2.0 * (double)n * n * (double)L.np;
+  if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + (refine ? 2.0 * (double)n * n * (double)L.np : 0.0);
   if (status != HP_OK) {
     set_error("syev: Jacobi iteration did not converge");
     return HP_ELINALG;
   }
-  // Rayleigh-quotient refinement: Y = G0 V (Y reuses the padded G buffer), rq_i = v_i . y_i
+  // Rayleigh-quotient refinement (refine != 0): Y = G0 V (Y reuses the padded G buffer),
+  // rq_i = v_i . y_i / v_i . v_i; otherwise the converged diagonal.  Padding columns -> -inf.
   {
-    VecSet a{G, ldg, nullptr};
-    VecSet b{p.V, L.np, nullptr};
-    const bool al16 = (ldg % 2 == 0) && ((uintptr_t)G % 16 == 0);
-    int rc = gemm_run(false, true, n, L.np, n, a, b, al16, 1.0, 0.0, p.G, L.np, nullptr, nullptr, nullptr, 0, 0,
-                      base + L.off_gemm, L.total - L.off_gemm, st);
-    if (rc) return rc;
     double* rq = reinterpret_cast<double*>(base + L.off_rq);
-    rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, L.np, rq);
+    if (refine) {
+      VecSet a{G, ldg, nullptr};
+      VecSet b{p.V, L.np, nullptr};
+      const bool al16 = (ldg % 2 == 0) && ((uintptr_t)G % 16 == 0);
+      int rc = gemm_run(false, true, n, L.np, n, a, b, al16, 1.0, 0.0, p.G, L.np, nullptr, nullptr, nullptr, 0, 0,
+                        base + L.off_gemm, L.total - L.off_gemm, st);
+      if (rc) return rc;
+      rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, L.np, rq);
+    } else {
+      rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, nullptr, 0, n, L.np, rq, p.G, L.np);
+    }
     HP_CHECK_LAUNCH("rq_diag");
     // rank all n_p columns (padding last), keep the first n
     sort_rank<<<(unsigned)ceil_div(L.np, 256), 256, 0, st>>>(rq, L.np, n, lam_desc, perm);

@@ -197,6 +197,36 @@ __global__ void max_diag_kernel(const double* d, int64_t m, double* out) {
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
+// y = G x (G symmetric, column-major): one thread per row, coalesced over columns
+__global__ void gemv_sym(const double* G, int64_t ldg, int64_t m, const double* x, double* y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int64_t j = 0; j < m; ++j) s += G[j * ldg + i] * x[j];
+  y[i] = s;
+}
+
+// x = y / ||y||, out = ||y|| (single CTA, fixed-order reduction)
+__global__ void normalise(const double* y, int64_t m, double* x, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += 256) s += y[i] * y[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  const double nrm = sqrt(red[0]);
+  for (int64_t i = threadIdx.x; i < m; i += 256) x[i] = nrm > 0.0 ? y[i] / nrm : 0.0;
+  if (threadIdx.x == 0) out[0] = nrm;
+}
+
+__global__ void fill_value(double* x, int64_t m, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) x[i] = v;
+}
+
 }  // namespace pc
 
 size_t pstrf_workspace_bytes(int64_t m) {
@@ -205,6 +235,7 @@ size_t pstrf_workspace_bytes(int64_t m) {
   size_t o = al((size_t)ld * m * 8);          // A
   o += al((size_t)m * 8);                       // d
   o += al(2048 * 8) + al(2048 * 4) + al(64);    // partials (2 x 1024) + rank + scal
+  o += 2 * al((size_t)m * 8);                   // power-iteration vectors
   o += al(gemm_workspace_bytes(m, m, pc::PB, 1, 0));
   return o;
 }
@@ -212,7 +243,7 @@ size_t pstrf_workspace_bytes(int64_t m) {
 // G (m x m) -> L (m x r, rows in original order), piv (r), rank r (host).
 // tol_rel: stop when the largest remaining pivot <= tol_rel * max_i |G_ii|.
 int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
-              int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+              double tol_lam, int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace pc;
   HP_REQUIRE(ws_bytes >= pstrf_workspace_bytes(m), "pstrf: workspace too small");
   *rank_out = 0;
@@ -231,7 +262,12 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   o += al(2048 * 4);
   int* rank = reinterpret_cast<int*>(base + o);
   double* scal = reinterpret_cast<double*>(base + o + 16);
+  double* lam_est = reinterpret_cast<double*>(base + o + 32);
   o += al(64);
+  double* px = reinterpret_cast<double*>(base + o);
+  o += al((size_t)m * 8);
+  double* py = reinterpret_cast<double*>(base + o);
+  o += al((size_t)m * 8);
   void* gws = base + o;
   const size_t gwsb = ws_bytes - o;
 
@@ -240,6 +276,19 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   max_diag_kernel<<<1, 256, 0, st>>>(d, m, scal);
   HP_CHECK_LAUNCH("max_diag");
   HP_CHECK_CUDA(cudaMemsetAsync(rank, 0, sizeof(int), st));
+  // lower bound of lambda_max by power iteration: ||G x|| <= lambda_max for ||x|| = 1
+  double host_lam = 0.0;
+  if (tol_lam > 0.0) {
+    fill_value<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(px, m, 1.0 / sqrt((double)m));
+    HP_CHECK_LAUNCH("fill_value");
+    for (int it = 0; it < 8; ++it) {
+      gemv_sym<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, m, px, py);
+      HP_CHECK_LAUNCH("gemv_sym");
+      normalise<<<1, 256, 0, st>>>(py, m, px, lam_est);
+      HP_CHECK_LAUNCH("normalise");
+    }
+    HP_CHECK_CUDA(cudaMemcpyAsync(&host_lam, lam_est, sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   double host_scal = 0.0;
   HP_CHECK_CUDA(cudaMemcpyAsync(&host_scal, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
   HP_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -264,7 +313,7 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   p.red_v = red_v;
   p.red_i = red_i;
   p.rank = rank;
-  p.tol = tol_rel * host_scal;
+  p.tol = std::max(tol_rel * host_scal, tol_lam * host_lam);
   int host_rank = 0;
   for (int64_t k0 = 0; k0 < m; k0 += PB) {
     p.k0 = (int)k0;

@@ -102,7 +102,7 @@ def test_syev_matches_eigh(n):
     V = D.DevMat.empty(n, n)
     w = ws(lib.hp_syev_workspace_bytes(n))
     sweeps = ctypes.c_int(0)
-    N.check(lib.hp_syev(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0, 0.0, 60,
+    N.check(lib.hp_syev(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0, 0.0, 60, 1,
                         ctypes.byref(sweeps), None, w.data_ptr(), w.numel(), st()), "syev")
     ev = lam_d.cpu().numpy()
     ref = np.linalg.eigvalsh(g)[::-1]
@@ -129,7 +129,7 @@ def test_syev_graded_psd_gram():
     V = D.DevMat.empty(m, m)
     w = ws(lib.hp_syev_workspace_bytes(m))
     sweeps = ctypes.c_int(0)
-    N.check(lib.hp_syev(G.ptr, G.ld, m, lam_d.data_ptr(), V.ptr, V.ld, m, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0, 0.0, 60,
+    N.check(lib.hp_syev(G.ptr, G.ld, m, lam_d.data_ptr(), V.ptr, V.ld, m, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0, 0.0, 60, 1,
                         ctypes.byref(sweeps), None, w.data_ptr(), w.numel(), st()), "syev")
     ev = lam_d.cpu().numpy()
     import scipy.linalg

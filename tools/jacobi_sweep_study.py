@@ -12,7 +12,7 @@ def run(g_dev, n, label):
     sw = ctypes.c_int(0)
     torch.cuda.synchronize(); t0 = time.perf_counter()
     N.check(lib.hp_syev(g_dev.ptr, g_dev.ld, n, lam.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0, 0.0,
-                        80, ctypes.byref(sw), None, ws.data_ptr(), ws.numel(), D._stream()), "syev")
+                        80, 1, ctypes.byref(sw), None, ws.data_ptr(), ws.numel(), D._stream()), "syev")
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
     print(f"{label:28s} n={n:5d} sweeps={sw.value:3d} time={dt*1e3:9.1f} ms", flush=True)
     return lam.cpu().numpy()

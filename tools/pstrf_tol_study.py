@@ -11,7 +11,7 @@ def ang(a, b):
 
 wl0 = W.make(0); q10 = W.haar_frame(wl0.d, 1000, 0, 1).cpu().numpy()
 wl1 = W.make(1, d=20000); q11 = W.haar_frame(wl1.d, 8192, 1, 1).cpu().numpy()
-for tol in [1e-12, 3e-12, 1e-11, 3e-11]:
+for tol in [2.0 ** -52]:
     D.PSTRF_TOL = tol
     try:
         H.pod(H.SnapshotBlock(H.InnerProductSpace(wl0.d), wl0.values), wl0.eps_star)
