@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,6 +60,7 @@ class Profiler:
 
     enabled = False
     records: list = []
+    _tag = threading.local()   # the node a thread is evaluating (set by evaluate_node)
 
     @classmethod
     def reset(cls, enabled=True):
@@ -66,12 +68,23 @@ class Profiler:
         cls.records = []
 
     @classmethod
-    def summary(cls):
-        """{phase: (launches, total_ms, total_flops)} -- synchronises the device."""
+    def set_tag(cls, tag):
+        cls._tag.value = tag
+
+    @classmethod
+    def tag(cls):
+        return getattr(cls._tag, "value", None)
+
+    @classmethod
+    def summary(cls, tag=None):
+        """{phase: (launches, total_ms, total_flops)} over all records (or those of one
+        tag, e.g. one node) -- synchronises the device."""
         out: dict = {}
         if cls.records:
             torch.cuda.synchronize()
-        for name, e0, e1, flops in cls.records:
+        for name, e0, e1, flops, t in cls.records:
+            if tag is not None and t != tag:
+                continue
             n, ms, f = out.get(name, (0, 0.0, 0.0))
             out[name] = (n + 1, ms + e0.elapsed_time(e1), f + flops)
         return out
@@ -95,7 +108,7 @@ class _phase:
         if self.e0 is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
-            Profiler.records.append((self.name, self.e0, e1, self.flops))
+            Profiler.records.append((self.name, self.e0, e1, self.flops, Profiler.tag()))
         return False
 
 
