@@ -72,6 +72,8 @@ __device__ __forceinline__ void tile_coords(const Params& p, int64_t t, int& bi,
   } else {
     bi = (int)(t % p.tiles_m);
     bj = (int)(t / p.tiles_m);
+    // upper-triangular B: tiles of later columns contract over longer K -- schedule them first
+    if (p.b_upper) bj = p.tiles_n - 1 - bj;
   }
 }
 
