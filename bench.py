@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--workers", type=int, default=None, help="stream workers for the leaf wave (N=1)")
     ap.add_argument("--cpu-leaves", type=int, default=2, help="leaves in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs only)")
     return ap.parse_args()
 
 
@@ -262,9 +263,12 @@ def main():
     clocks.start()
     ms, out, launches, summ = timed(step_device, a.steps, profile=True)
     clk = clocks.stop()
-    for _ in range(max(1, a.warmup // 3)):
-        step_e2e()
-    ms_e2e, out_e2e, _, _ = timed(step_e2e, a.steps)
+    if a.no_e2e:
+        ms_e2e = float("nan")
+    else:
+        for _ in range(max(1, a.warmup // 3)):
+            step_e2e()
+        ms_e2e, out_e2e, _, _ = timed(step_e2e, a.steps)
 
     cols_per_s = m * a.steps / (ms * 1e-3)
     e2e_cols = m * a.steps / (ms_e2e * 1e-3)
