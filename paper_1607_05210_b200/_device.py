@@ -263,8 +263,8 @@ def _concat_parts(parts: list[Part]):
     """VecSet over the concatenated columns + the concatenated scale (or None)."""
     parts = [p for p in parts if p.mat.cols]
     m = sum(p.mat.cols for p in parts)
-    if len(parts) == 1 and parts[0].scale is None:
-        return parts[0].mat.vecset(), None, m, parts
+    if len(parts) == 1:
+        return parts[0].mat.vecset(), parts[0].scale, m, parts
     table = np.empty(m, dtype=np.int64)
     at = 0
     aligned = True
@@ -280,6 +280,35 @@ def _concat_parts(parts: list[Part]):
         scale = torch.cat([p.scale if p.scale is not None else ones(p.mat.cols) for p in parts])
     vs = N.VecSet(0, 0, tdev.data_ptr(), int(aligned))
     return vs, scale, m, (parts, tdev)
+
+
+PACK_MIN_PARTS = 4   # inputs with this many column blocks are packed into one matrix
+
+
+def pack_parts(parts: list[Part]) -> list[Part]:
+    """A node input of many column blocks (an interior node's children) as ONE column-major
+    matrix + the concatenated per-column scale, so the Gram and reconstruction GEMMs read it
+    with tensor TMA instead of through a pointer table.  The copy moves 2 d m 8 bytes (a few ms
+    at the config-1 root against ~1 s of contractions).  Inputs with fewer blocks are returned
+    unchanged."""
+    live = [p for p in parts if p.mat.cols]
+    if len(live) < PACK_MIN_PARTS:
+        return parts
+    lib = N.load()
+    d = live[0].mat.rows
+    m = sum(p.mat.cols for p in live)
+    out = DevMat.empty(d, m)
+    at = 0
+    dst = out.storage[: out.ld * m].view(m, out.ld)
+    for p in live:
+        c = p.mat.cols
+        src = p.mat.storage[p.mat.offset: p.mat.offset + p.mat.ld * c].view(c, p.mat.ld)
+        dst[at: at + c, :d].copy_(src[:, :d])
+        at += c
+    scale = None
+    if any(p.scale is not None for p in live):
+        scale = torch.cat([p.scale if p.scale is not None else ones(p.mat.cols) for p in live])
+    return [Part(out, scale)]
 
 
 def weigh_parts(parts: list[Part], sqrt_w) -> list[Part]:
@@ -531,10 +560,29 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     else:
         Vs = Vn
     U = DevMat.empty(d, n_modes)
-    ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
-    with _phase("assemble", 2.0 * d * m * n_modes):
-        N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld,
-                                ws.data_ptr(), ws.numel(), st), "assemble")
+    live = [p for p in parts if p.mat.cols]
+    if len(live) <= 1:
+        ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
+        with _phase("assemble", 2.0 * d * m * n_modes):
+            N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld,
+                                    ws.data_ptr(), ws.numel(), st), "assemble")
+    else:
+        # a few column blocks (an incremental merge [Phi sigma | F]): U = sum_p S_p (V_p / sigma),
+        # one plain-operand (TMA) GEMM per block accumulating into U -- no pointer table
+        rsig = 1.0 / sig_dev
+        ws = _ws(max(lib.hp_gemm_workspace_bytes(d, n_modes, p.mat.cols, 0, 0) for p in live))
+        with _phase("assemble", 2.0 * d * m * n_modes):
+            r0 = 0
+            for i, p in enumerate(live):
+                c = p.mat.cols
+                Vp = DevMat.empty(c, n_modes)  # rows r0..r0+c of V / sigma, 16-byte aligned columns
+                N.check(lib.hp_scale(Vs.ptr + 8 * r0, Vs.ld, c, n_modes, None, None, rsig.data_ptr(), Vp.ptr, Vp.ld,
+                                     st), "V / sigma")
+                N.check(lib.hp_gemm(0, 1, d, n_modes, c, p.mat.vecset(), Vp.vecset(), 1.0, 0.0 if i == 0 else 1.0,
+                                    U.ptr, U.ld, None, None, None, 0, 0, ws.data_ptr(), ws.numel(), st),
+                        "assemble part")
+                r0 += c
+        del rsig
     del ws, Vs
     # drift = max |U^T W U - I| (U is in Euclidean coordinates when weighted)
     C = DevMat.empty(n_modes, n_modes)
@@ -576,6 +624,8 @@ def node_pod(parts: list[Part], d: int, eps: float, cutoff: float, want_right: b
     """Full device pod() of the concatenated parts (pod.py:328-337)."""
     if sqrt_w is not None:
         parts = weigh_parts(parts, sqrt_w)
+    with _phase("pack"):
+        parts = pack_parts(parts)
     G, m, _keep = gram_full(parts, d)
     return spectrum_and_modes(G, m, parts, d, eps, cutoff, want_right, sqrt_w)
 

@@ -24,6 +24,10 @@
 // run and independent of how many GPUs take part (no atomics).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "hp_common.cuh"
 
@@ -118,6 +122,107 @@ __device__ __forceinline__ void load_operand(double* s, const VecSet& op, int64_
   }
 }
 
+// One BK-deep k tile of the 128x128 CTA tile: this warp's 64x32 sub-tile, DMMA m8n8k4.
+template <bool AK, bool BKM>
+__device__ __forceinline__ void mma_ktile(const double* as, const double* bs, double (&acc)[8][4][2], int wm, int wn,
+                                          int g, int t) {
+  using L = Layout<AK, BKM>;
+  if (L::MODEP) {
+#pragma unroll
+    for (int sp = 0; sp < 2; ++sp) {
+      double2 af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        af[i] = *reinterpret_cast<const double2*>(as + (wm * 64 + i * 8 + g) * L::LDK + 4 * t + 2 * sp);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        bf[j] = *reinterpret_cast<const double2*>(bs + (wn * 32 + j * 8 + g) * L::LDK + 4 * t + 2 * sp);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
+        }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
+        }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      double af[8], bf[4];
+      const int kk = 4 * s + t;
+      if (AK) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) af[i] = as[(wm * 64 + i * 8 + g) * L::LDK + kk];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double2 v = *reinterpret_cast<const double2*>(as + kk * LDM + wm * 64 + g * 8 + 2 * q);
+          af[2 * q] = v.x;
+          af[2 * q + 1] = v.y;
+        }
+      }
+      if (BKM) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = bs[(wn * 32 + j * 8 + g) * L::LDK + kk];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double2 v = *reinterpret_cast<const double2*>(bs + kk * LDM + wn * 32 + g * 4 + 2 * q);
+          bf[2 * q] = v.x;
+          bf[2 * q + 1] = v.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+  }
+}
+
+// Epilogue: split-K partial tile, or alpha/beta/row-col scale/divide + symmetric mirror into C.
+template <bool AK, bool BKM>
+__device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8][4][2], int64_t tile, int z, int64_t m0,
+                                         int64_t n0, int wm, int wn, int g, int t) {
+  if (p.splits > 1) {
+    double* out = p.partial + ((int64_t)z * p.ntiles + tile) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ml = wm * 64 + (AK ? i * 8 + g : g * 8 + i);
+          const int nl = wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+          out[nl * BM + ml] = acc[i][j][e];
+        }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t m = m0 + wm * 64 + (AK ? i * 8 + g : g * 8 + i);
+        const int64_t n = n0 + wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+        if (m >= p.M || n >= p.N) continue;
+        if (p.sym && m > n) continue;
+        double v = p.alpha * acc[i][j][e];
+        if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
+        if (p.row_scale) v *= p.row_scale[m];
+        if (p.col_scale) v *= p.col_scale[n];
+        if (p.col_div) v /= p.col_div[n];
+        p.C[n * p.ldc + m] = v;
+        if (p.sym && m != n) p.C[m * p.ldc + n] = v;
+      }
+}
+
 template <bool AK, bool BKM, bool VEC>
 __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(Params p) {
   using L = Layout<AK, BKM>;
@@ -164,100 +269,184 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(Params p) {
     if (nxt < nk) load_stage(nxt % STAGES, kbeg + (int64_t)nxt * BK);
     cp_async_commit();
 
-    const double* as = stage_a(kt % STAGES);
-    const double* bs = stage_b(kt % STAGES);
-    if (L::MODEP) {
-#pragma unroll
-      for (int sp = 0; sp < 2; ++sp) {
-        double2 af[8], bf[4];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          af[i] = *reinterpret_cast<const double2*>(as + (wm * 64 + i * 8 + g) * L::LDK + 4 * t + 2 * sp);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          bf[j] = *reinterpret_cast<const double2*>(bs + (wn * 32 + j * 8 + g) * L::LDK + 4 * t + 2 * sp);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
-          }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
-          }
-      }
-    } else {
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        double af[8], bf[4];
-        const int kk = 4 * s + t;
-        if (AK) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) af[i] = as[(wm * 64 + i * 8 + g) * L::LDK + kk];
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            double2 v = *reinterpret_cast<const double2*>(as + kk * LDM + wm * 64 + g * 8 + 2 * q);
-            af[2 * q] = v.x;
-            af[2 * q + 1] = v.y;
-          }
-        }
-        if (BKM) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bf[j] = bs[(wn * 32 + j * 8 + g) * L::LDK + kk];
-        } else {
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            double2 v = *reinterpret_cast<const double2*>(bs + kk * LDM + wn * 32 + g * 4 + 2 * q);
-            bf[2 * q] = v.x;
-            bf[2 * q + 1] = v.y;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
-      }
-    }
+    mma_ktile<AK, BKM>(stage_a(kt % STAGES), stage_b(kt % STAGES), acc, wm, wn, g, t);
   }
   cp_async_wait<0>();
 
-  // ---------------------------------------------------------------- epilogue
-  if (p.splits > 1) {
-    double* out = p.partial + ((int64_t)z * p.ntiles + tile) * (BM * BN);
+  epilogue<AK, BKM>(p, acc, tile, z, m0, n0, wm, wn, g, t);
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA-staged variant (plain strided operands, 16-byte aligned): warp 8 is the producer and
+// moves every operand tile with tensor TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B, hardware
+// zero fill outside the matrix); warps 0-7 consume.  Each of the TSTAGES ring slots has a
+// "full" mbarrier (producer arrive + transaction bytes) and an "empty" mbarrier (one arrive
+// per consumer warp): no CTA-wide barrier and no load instruction in the main loop of the
+// consumer warps, and no edge code at all (partial tiles in M, N and K are zero-filled by the
+// TMA unit).
+//   K-major operand : one box {16 k, 128 vectors}: row r = 128 B, 16-byte chunk c of row r
+//                     stored at chunk c ^ (r & 7)
+//   M-major operand : 8 boxes {16 m, 16 k}: box b holds m in [16b, 16b+16), k-row kk = 128 B,
+//                     chunk c of row kk stored at c ^ (kk & 7)
+// With these swizzles the fragment loads of both the 128-bit (both K-major) and the M-major
+// paths are bank-conflict free.
+constexpr int TSTAGES = 6, TTHREADS = 384;  // 2 consumer warpgroups + 1 producer warpgroup
+constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
+
+struct TmaParams {
+  CUtensorMap ta, tb;  // 64-byte aligned (CUtensorMap is declared alignas(64))
+  Params p;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// byte offset of element (row, k) in a K-major tile / (m, k) in an M-major tile
+__device__ __forceinline__ int kmaj_off(int row, int k) {
+  return row * 128 + ((((k >> 1) ^ row) & 7) << 4) + (k & 1) * 8;
+}
+__device__ __forceinline__ int mmaj_off(int m, int k) {
+  return (m >> 4) * 2048 + k * 128 + (((((m & 15) >> 1) ^ k) & 7) << 4) + (m & 1) * 8;
+}
+
+template <bool AK, bool BKM>
+__device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, double (&acc)[8][4][2], int wm, int wn,
+                                             int g, int t) {
+  if (AK && BKM) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int sp = 0; sp < 2; ++sp) {
+      double2 af[8], bf[4];
+      const int kk = 4 * t + 2 * sp;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double2*>(as + kmaj_off(wm * 64 + i * 8 + g, kk));
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int ml = wm * 64 + (AK ? i * 8 + g : g * 8 + i);
-          const int nl = wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
-          out[nl * BM + ml] = acc[i][j][e];
+      for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double2*>(bs + kmaj_off(wn * 32 + j * 8 + g, kk));
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      double af[8], bf[4];
+      const int kk = 4 * s + t;
+      if (AK) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double*>(as + kmaj_off(wm * 64 + i * 8 + g, kk));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(as + mmaj_off(wm * 64 + g * 8 + 2 * q, kk));
+          af[2 * q] = v.x;
+          af[2 * q + 1] = v.y;
         }
+      }
+      if (BKM) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double*>(bs + kmaj_off(wn * 32 + j * 8 + g, kk));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(bs + mmaj_off(wn * 32 + g * 4 + 2 * q, kk));
+          bf[2 * q] = v.x;
+          bf[2 * q + 1] = v.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+  }
+}
+
+template <bool AK, bool BKM>
+__global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
+  const Params& p = tp.p;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full_bar[TSTAGES], empty_bar[TSTAGES];
+  // 128B-swizzled TMA destinations must be 1024-byte aligned
+  char* sbase = reinterpret_cast<char*>(smem) + ((1024u - (smem_u32(smem) & 1023u)) & 1023u);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  const int64_t tile = blockIdx.x;
+  const int z = blockIdx.z;
+  int bi, bj;
+  tile_coords(p, tile, bi, bj);
+  const int64_t m0 = (int64_t)bi * BM, n0 = (int64_t)bj * BN;
+  const int64_t kbeg = (int64_t)z * p.kspan;
+  int64_t kend = min(p.K, kbeg + p.kspan);
+  if (p.b_upper) kend = min(kend, n0 + BN);
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp >= 8) {
+    // ------------------------------------------------------------------ producer
+    // the producer warpgroup hands its registers to the consumers (setmaxnreg: per-SMSP
+    // register files hold 2 consumer warps at 224 + 1 producer warp at 56)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp != 8 || lane != 0) return;
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TSTAGES;
+      if (kt >= TSTAGES) mbar_wait(&empty_bar[s], ((kt / TSTAGES) - 1) & 1);
+      const int k0 = (int)(kbeg + (int64_t)kt * BK);
+      char* sa = sbase + s * 2 * TILE_BYTES;
+      char* sb = sa + TILE_BYTES;
+      mbar_arrive_expect_tx(&full_bar[s], 2 * TILE_BYTES);
+      if (AK) {
+        tma_load_2d(sa, &tp.ta, k0, (int)m0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < BM / 16; ++b) tma_load_2d(sa + b * 2048, &tp.ta, (int)m0 + 16 * b, k0, &full_bar[s]);
+      }
+      if (BKM) {
+        tma_load_2d(sb, &tp.tb, k0, (int)n0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, &tp.tb, (int)n0 + 16 * b, k0, &full_bar[s]);
+      }
+    }
     return;
   }
+
+  // -------------------------------------------------------------------- consumers (warps 0-7)
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[8][4][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t m = m0 + wm * 64 + (AK ? i * 8 + g : g * 8 + i);
-        const int64_t n = n0 + wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
-        if (m >= p.M || n >= p.N) continue;
-        if (p.sym && m > n) continue;
-        double v = p.alpha * acc[i][j][e];
-        if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
-        if (p.row_scale) v *= p.row_scale[m];
-        if (p.col_scale) v *= p.col_scale[n];
-        if (p.col_div) v /= p.col_div[n];
-        p.C[n * p.ldc + m] = v;
-        if (p.sym && m != n) p.C[m * p.ldc + n] = v;
-      }
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TSTAGES;
+    mbar_wait(&full_bar[s], (kt / TSTAGES) & 1);
+    const char* sa = sbase + s * 2 * TILE_BYTES;
+    mma_ktile_sw<AK, BKM>(sa, sa + TILE_BYTES, acc, wm, wn, g, t);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+  epilogue<AK, BKM>(p, acc, tile, z, m0, n0, wm, wn, g, t);
 }
 
 // Fixed-order split-K reduction + epilogue.  One thread per tile element.
@@ -328,6 +517,60 @@ int launch_t(const Params& p, cudaStream_t st) {
   return HP_OK;
 }
 
+constexpr int TMA_SMEM = TSTAGES * 2 * TILE_BYTES + 1024;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 2-d map over `outer` vectors of `inner` contiguous float64 (vector stride ld elements)
+bool encode_map(CUtensorMap* map, const double* base, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                int box_outer) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(inner, 1), (cuuint64_t)std::max<int64_t>(outer, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool AK, bool BKM>
+int launch_tma(const Params& p, cudaStream_t st, bool& done) {
+  done = false;
+  static bool configured = false;
+  TmaParams tp;
+  tp.p = p;
+  // K-major: inner = K (contiguous k of each vector), outer = M / N vectors, box {16, 128}
+  // M-major: inner = M / N (contiguous rows of each k-vector), outer = K, box {16, 16}
+  const bool ok_a = AK ? encode_map(&tp.ta, p.A.base, p.K, p.M, p.A.ld, BK, BM)
+                       : encode_map(&tp.ta, p.A.base, p.M, p.K, p.A.ld, 16, BK);
+  const bool ok_b = BKM ? encode_map(&tp.tb, p.B.base, p.K, p.N, p.B.ld, BK, BN)
+                        : encode_map(&tp.tb, p.B.base, p.N, p.K, p.B.ld, 16, BK);
+  if (!ok_a || !ok_b) return HP_OK;  // not encodable: caller uses the cp.async kernel
+  if (!configured) {
+    HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TMA_SMEM));
+    configured = true;
+  }
+  dim3 grid((unsigned)p.ntiles, 1, (unsigned)p.splits);
+  gemm_tma_kernel<AK, BKM><<<grid, TTHREADS, TMA_SMEM, st>>>(tp);
+  HP_CHECK_LAUNCH("gemm_tma_kernel");
+  done = true;
+  return HP_OK;
+}
+
 }  // namespace gemm
 
 // Host entry used by the C-ABI and by the other modules.
@@ -370,7 +613,21 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
     }
   }
   int rc;
-  if (a_kmajor && b_kmajor)
+  static const bool use_tma = !(getenv("HP_GEMM_TMA") && atoi(getenv("HP_GEMM_TMA")) == 0);
+  bool done = false;
+  rc = HP_OK;
+  if (aligned16 && use_tma && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31)) {
+    if (a_kmajor && b_kmajor)
+      rc = launch_tma<true, true>(p, st, done);
+    else if (!a_kmajor && b_kmajor)
+      rc = launch_tma<false, true>(p, st, done);
+    else if (!a_kmajor && !b_kmajor)
+      rc = launch_tma<false, false>(p, st, done);
+    else
+      rc = launch_tma<true, false>(p, st, done);
+  }
+  if (rc || done) {
+  } else if (a_kmajor && b_kmajor)
     rc = aligned16 ? launch_t<true, true, true>(p, st) : launch_t<true, true, false>(p, st);
   else if (!a_kmajor && b_kmajor)
     rc = aligned16 ? launch_t<false, true, true>(p, st) : launch_t<false, true, false>(p, st);

@@ -90,6 +90,34 @@ def test_gemm_nt_sym_and_upper():
     assert np.allclose(Y.to_numpy(), x @ l.T, rtol=1e-12, atol=1e-11)
 
 
+@pytest.mark.parametrize("ak,bk", [(1, 1), (0, 1), (0, 0), (1, 0)])
+@pytest.mark.parametrize("M,N_,K", [(1, 1, 1), (130, 257, 37), (256, 128, 40_001), (517, 300, 16), (64, 700, 4098)])
+def test_gemm_layouts_edges(ak, bk, M, N_, K):
+    """Every operand layout of the GEMM engine (the TMA-staged kernel for 16-byte aligned
+    operands): partial edge tiles in M and N, a partial last k tile (K % 16 != 0, staged with
+    zero fill), split-K with the fixed-order reduction, and a pointer-table operand."""
+    rng = np.random.default_rng(M * 31 + N_ * 7 + K + 1000 * ak + 100 * bk)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N_))
+    A = D.upload(np.asfortranarray(a.T) if ak else a)     # K-major: vectors m with contiguous k
+    B = D.upload(b if bk else np.asfortranarray(b.T))     # K-major: vectors n with contiguous k
+    ref = a @ b
+    tol = 1e-13 * np.sqrt(K) * max(1.0, np.abs(ref).max())
+    for table in (False, True):
+        if table:
+            # the same operands addressed through per-vector pointer tables (children's mode blocks)
+            va, ta = D._concat_parts([D.Part(A.view_cols(0, A.cols // 2)), D.Part(A.view_cols(A.cols // 2, A.cols))])[::3]
+            vb, tb = D._concat_parts([D.Part(B.view_cols(0, B.cols // 3)), D.Part(B.view_cols(B.cols // 3, B.cols))])[::3]
+        else:
+            va, vb = A.vecset(), B.vecset()
+        C = D.DevMat.empty(M, N_)
+        w = ws(lib.hp_gemm_workspace_bytes(M, N_, K, 0, 0))
+        N.check(lib.hp_gemm(ak, bk, M, N_, K, va, vb, 1.0, 0.0, C.ptr, C.ld, None, None, None, 0, 0,
+                            w.data_ptr(), w.numel(), st()), "gemm")
+        err = np.abs(C.to_numpy() - ref).max()
+        assert err <= tol, (table, err, tol)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 64, 65, 200, 512, 1000])
 def test_syev_matches_eigh(n):
     rng = np.random.default_rng(n)
