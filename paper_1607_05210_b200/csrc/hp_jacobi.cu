@@ -63,6 +63,7 @@ struct Params {
   int* counter;       // pairs that needed work in this sweep
   double* maxoff;     // max |g_ij| / max|g_ii| seen in this sweep (atomic max on the bit pattern)
   unsigned long long* mm_count;  // 64x64x64 DMMA products performed by jac_apply (flop accounting)
+  unsigned long long* task_counter;  // dynamic task scheduler of the "rest" apply pass
   const double* scal; // scal[0] = max |g_ii| of the input
   double tol_rel, tol_abs;
   double keep_floor;  // pairs whose diagonal entries are both below this never rotate
@@ -156,17 +157,19 @@ __device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2
       for (int e = 0; e < 2; ++e) C[(c0 + j * 8 + 2 * t + e) * SC + r0 + i * 8 + g] = acc[i][j][e];
 }
 
-__global__ void __launch_bounds__(LT) jac_local(Params p) {
-  extern __shared__ double sm[];
+// One pair's local solve (block k of round p.round) by a CTA of NT threads (NT/32 warps; warp w
+// owns row pairs w, w + NT/32, ... and W rows w, w + NT/32, ...).  `sm` holds 3 PS x LS doubles.
+template <int NT>
+__device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) {
+  constexpr int NW = NT / 32;
   // A is double-buffered (each rotation step reads one copy and writes the other, so one
   // barrier per step suffices); W is column-major (Wl[j*LS + i] = w_ij) and its rows are
-  // owned by warps (row % 16 == warp), so W needs only __syncwarp between steps.
+  // owned by warps (row % NW == warp), so W needs only __syncwarp between steps.
   double* Acur = sm;
   double* Anx = sm + PS * LS;
   double* Wl = sm + 2 * PS * LS;
   __shared__ int sperm[PS];
 
-  const int k = blockIdx.x;
   int bp, bq;
   block_pair(p, k, bp, bq);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
   // not chase them; with a relative trigger (tol_abs tiny) the local solve follows it
   const double tloc = fmin(2.220446049250313e-16 * p.scal[0], ta);
 
-  for (int e = tid; e < PS * PS; e += LT) {
+  for (int e = tid; e < PS * PS; e += NT) {
     const int j = e / PS, i = e % PS;
     Acur[i * LS + j] = p.G[local_index(bp, bq, j) * p.np + local_index(bp, bq, i)];
   }
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
   // anything to do?  |g_ij| > max(tol_abs * max|g_ii|, tol_rel * sqrt|g_ii g_jj|)
   int mine = 0;
   double moff = 0.0;
-  for (int e = tid; e < PS * PS; e += LT) {
+  for (int e = tid; e < PS * PS; e += NT) {
     const int i = e / PS, j = e % PS;
     if (i < j) {
       const double aij = Acur[i * LS + j];
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     if (tid == 0) p.flags[k] = 0;
     return;
   }
-  for (int e = tid; e < PS * PS; e += LT) {
+  for (int e = tid; e < PS * PS; e += NT) {
     const int j = e / PS, i = e % PS;
     Wl[j * LS + i] = (i == j) ? 1.0 : 0.0;
   }
@@ -218,20 +221,18 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
       const int r = needs_rotation(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
       double c = 1.0, s = 0.0, t = 0.0;
       if (r) {
-        const double theta = (ajj - aii) / (2.0 * aij);
-        if (fabs(theta) > 1e150) {
-          t = 0.5 / theta;
-        } else {
-          t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-        }
-        c = rsqrt(1.0 + t * t);
+        // t = sgn(theta) / (|theta| + sqrt(1 + theta^2)), theta = (ajj - aii) / (2 aij), written
+        // with one square root and one division: t = 2 aij sgn(d) / (|d| + sqrt(d^2 + 4 aij^2))
+        const double dd = ajj - aii, a2 = 2.0 * aij;
+        t = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
+        c = rsqrt(fma(t, t, 1.0));
         s = t * c;
       }
       rotated |= r;
       // A_next = R^T A R : this warp owns row pairs P = warp and warp + 16, column pair Q = lane
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int P = warp + 16 * h;
+      for (int h = 0; h < 32 / NW; ++h) {
+        const int P = warp + NW * h;
         const int rp = __shfl_sync(0xffffffffu, r, P);
         const double cp = __shfl_sync(0xffffffffu, c, P), sp = __shfl_sync(0xffffffffu, s, P);
         const int i1 = __shfl_sync(0xffffffffu, a, P), j1 = __shfl_sync(0xffffffffu, b, P);
@@ -275,8 +276,8 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
       // W <- W R on this warp's rows
       if (r) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int row = warp + 16 * h;
+        for (int h = 0; h < 64 / NW; ++h) {
+          const int row = warp + NW * h;
           const double wi = Wl[a * LS + row], wj = Wl[b * LS + row];
           Wl[a * LS + row] = c * wi - s * wj;
           Wl[b * LS + row] = s * wi + c * wj;
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     __syncthreads();
     if (warp < 8) store_acc<LS>(E, acc);
     __syncthreads();
-    for (int e = tid; e < PS; e += LT) E[e * LS + e] -= 1.0;
+    for (int e = tid; e < PS; e += NT) E[e * LS + e] -= 1.0;
     __syncthreads();
     if (warp < 8) mm64<false, LS, LS>(Wl, E, acc);  // A(m,k) = Wl[k*LS+m] = W(m,k), B(k,n) = E(k,n)
     __syncthreads();
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     }
     __syncthreads();
   }
-  for (int e = tid; e < PS * PS; e += LT) {
+  for (int e = tid; e < PS * PS; e += NT) {
     const int j = e / PS, i = e % PS;
     p.W[(int64_t)k * PS * PS + j * PS + i] = Wn[sperm[j] * LS + i];
   }
@@ -339,6 +340,11 @@ __global__ void __launch_bounds__(LT) jac_local(Params p) {
     p.flags[k] = 1;
     atomicAdd(p.counter, 1);
   }
+}
+
+__global__ void __launch_bounds__(LT) jac_local(Params p) {
+  extern __shared__ double sm[];
+  local_solve<LT>(p, blockIdx.x, sm);
 }
 
 // async 16-byte copies: a 64x64 column-major W (contiguous) into smem stride TS
@@ -445,6 +451,8 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
   }
 }
 
+__device__ __forceinline__ void rest_tasks(const Params& p, double* X, double* WQ, double* WP);
+
 // Persistent apply: a fixed grid (2 CTAs per SM) walks all tasks; tasks of pairs that
 // needed no rotation cost two flag loads instead of a CTA launch.
 __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
@@ -455,6 +463,7 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
   const int npairs = p.nb / 2;
   const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
   if (p.phase == 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.task_counter = 0ull;  // for the "rest" pass that follows
     // the tiles the next round's local solves read: every pair's diagonal tile and, for each
     // pair (x, y) of round r+1, the tile holding block (x, y); claimed with the round stamp
     __shared__ int go;
@@ -479,16 +488,46 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
     }
     return;
   }
+  rest_tasks(p, X, WQ, WP);
+}
+
+// The "rest" apply pass of round p.round: every G tile / V slab not already applied by the
+// "needed" pass, dynamically scheduled.
+__device__ __forceinline__ void rest_tasks(const Params& p, double* X, double* WQ, double* WP) {
+  const int npairs = p.nb / 2;
+  const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
   const int64_t ntasks = ng + (p.np / PS) * npairs;
-  // contiguous chunk per CTA: consecutive tasks mostly share the column pair Q, whose
-  // rotation then stays in shared memory
-  const int64_t chunk = (ntasks + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = blockIdx.x * chunk, b1 = min(ntasks, b0 + chunk);
+  // dynamic scheduling in chunks of consecutive tasks (which mostly share the column pair Q, whose
+  // rotation then stays in shared memory): the heavy G tiles (two 64^3 products) come first, the
+  // V slabs (one product) last, and CTAs sharing an SM with a local solve simply take fewer chunks
+  constexpr int CH = 4;
+  __shared__ long long s_next;
   int wq_loaded = -1;
-  for (int64_t b = b0; b < b1; ++b) {
-    apply_task(p, b, ng, npairs, X, WQ, WP, wq_loaded);
-    __syncthreads();  // smem reuse by the next task
+  for (;;) {
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.task_counter, (unsigned long long)CH);
+    __syncthreads();
+    const int64_t b0 = s_next;
+    __syncthreads();
+    if (b0 >= ntasks) break;
+    const int64_t b1 = min(ntasks, b0 + CH);
+    for (int64_t b = b0; b < b1; ++b) {
+      apply_task(p, b, ng, npairs, X, WQ, WP, wq_loaded);
+      __syncthreads();  // smem reuse by the next task
+    }
   }
+}
+
+// One Jacobi round after its "needed" pass: CTAs 0..npairs-1 first solve the local problems of
+// round r+1 (they only read tiles the needed pass of round r has finished), then every CTA takes
+// chunks of round r's remaining apply tasks.  One launch, one stream: the local solves (the
+// round's critical path) start at once and the apply fills the SMs around them.
+__global__ void __launch_bounds__(AT, 2) jac_round(Params pa, Params pl, int do_local, int do_rest) {
+  extern __shared__ double sm[];
+  if (do_local && blockIdx.x < pl.nb / 2) {
+    local_solve<AT>(pl, blockIdx.x, sm);
+    __syncthreads();
+  }
+  if (do_rest) rest_tasks(pa, sm, sm + PS * TS, sm + 2 * PS * TS);
 }
 
 __global__ void pad_copy(const double* G, int64_t ldg, int64_t n, double* Gp, double* Vp, int64_t np) {
@@ -627,6 +666,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.counter = reinterpret_cast<int*>(base + L.off_counter);
   p.maxoff = reinterpret_cast<double*>(base + L.off_counter + 16);
   p.mm_count = reinterpret_cast<unsigned long long*>(base + L.off_counter + 24);
+  p.task_counter = reinterpret_cast<unsigned long long*>(base + L.off_counter + 32);
   double* scal = reinterpret_cast<double*>(base + L.off_scal);
   p.scal = scal;
   int* perm = reinterpret_cast<int*>(base + L.off_perm);
@@ -644,6 +684,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   const int apply_smem = 3 * PS * TS * 8;
   if (!configured) {
     HP_CHECK_CUDA(cudaFuncSetAttribute(jac_local, cudaFuncAttributeMaxDynamicSharedMemorySize, local_smem));
+    HP_CHECK_CUDA(cudaFuncSetAttribute(jac_round, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem));
     HP_CHECK_CUDA(cudaFuncSetAttribute(jac_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem));
     configured = true;
   }
@@ -671,13 +712,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   cudaEvent_t ev[3];
   if (trace > 1)
     for (auto& e : ev) cudaEventCreate(&e);
-  // Two streams: round r+1's local solves (stream st2) overlap round r's "rest" apply pass
-  // (stream st); they only need the tiles of round r's "needed" pass.
-  cudaStream_t st2 = nullptr;
-  cudaEvent_t e_needed = nullptr, e_local = nullptr;
-  HP_CHECK_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  HP_CHECK_CUDA(cudaEventCreateWithFlags(&e_needed, cudaEventDisableTiming));
-  HP_CHECK_CUDA(cudaEventCreateWithFlags(&e_local, cudaEventDisableTiming));
+  static const bool use_fused = !(getenv("HP_JACOBI_FUSED") && atoi(getenv("HP_JACOBI_FUSED")) == 0);
   HP_CHECK_CUDA(cudaMemsetAsync(p.tile_mark, 0, (size_t)npairs * (npairs + 1) / 2 * 4, st));
   const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, nsm);
   const unsigned rest_grid = (unsigned)std::min<int64_t>(napply, 2 * (int64_t)nsm);
@@ -685,33 +720,47 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   for (; sweep < max_sweeps; ++sweep) {
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
     if (e != cudaSuccess) break;
-    cudaEventRecord(e_needed, st);
-    for (int r = 0; r < L.nb - 1; ++r) {
-      p.round = r;
-      p.W = W_base + (size_t)(r & 1) * npairs * PS * PS;
-      p.flags = flags_base + (size_t)(r & 1) * npairs;
-      p.stamp = ++stamp;
-      cudaStreamWaitEvent(st2, e_needed, 0);
-      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[0], st2);
-      jac_local<<<npairs, LT, local_smem, st2>>>(p);
-      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[1], st2);
-      cudaEventRecord(e_local, st2);
-      cudaStreamWaitEvent(st, e_local, 0);
-      p.phase = 1;
-      jac_apply<<<needed_grid, AT, apply_smem, st>>>(p);
-      cudaEventRecord(e_needed, st);
-      p.phase = 2;
-      jac_apply<<<rest_grid, AT, apply_smem, st>>>(p);
-      if (trace > 1 && r == L.nb / 2) cudaEventRecord(ev[2], st);
-      count_launches(3);
+    // Per round r: needed(r), then ONE fused launch in which CTAs 0..npairs-1 solve the local
+    // problems of round r+1 before joining the dynamically scheduled rest of round r's apply.
+    const int R = L.nb - 1;
+    auto round_params = [&](int r) {
+      Params q = p;
+      q.round = r;
+      q.W = W_base + (size_t)(r & 1) * npairs * PS * PS;
+      q.flags = flags_base + (size_t)(r & 1) * npairs;
+      q.stamp = stamp + r + 1;
+      return q;
+    };
+    if (use_fused) {
+      jac_round<<<npairs, AT, apply_smem, st>>>(round_params(0), round_params(0), 1, 0);
+    } else {
+      jac_local<<<npairs, LT, local_smem, st>>>(round_params(0));
     }
+    for (int r = 0; r < R; ++r) {
+      Params q = round_params(r);
+      q.phase = 1;
+      jac_apply<<<needed_grid, AT, apply_smem, st>>>(q);
+      if (trace > 1 && r == R / 2) cudaEventRecord(ev[0], st);
+      q.phase = 2;
+      if (use_fused) {
+        jac_round<<<rest_grid, AT, apply_smem, st>>>(q, round_params(r + 1 < R ? r + 1 : 0), r + 1 < R, 1);
+        count_launches(2);
+      } else {
+        jac_apply<<<rest_grid, AT, apply_smem, st>>>(q);
+        if (trace > 1 && r == R / 2) cudaEventRecord(ev[1], st);
+        if (r + 1 < R) jac_local<<<npairs, LT, local_smem, st>>>(round_params(r + 1));
+        count_launches(3);
+      }
+      if (trace > 1 && r == R / 2) {
+        if (use_fused) cudaEventRecord(ev[1], st);
+        cudaEventRecord(ev[2], st);
+      }
+    }
+    stamp += R;
     e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       cudaFreeHost(host_buf);
-      cudaEventDestroy(e_needed);
-      cudaEventDestroy(e_local);
-      cudaStreamDestroy(st2);
       set_error(std::string("syev sweep: ") + cudaGetErrorString(e));
       return HP_ECUDA;
     }
@@ -734,9 +783,6 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     prev_off = off;
   }
   cudaFreeHost(host_buf);
-  cudaEventDestroy(e_needed);
-  cudaEventDestroy(e_local);
-  cudaStreamDestroy(st2);
   if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
   // algorithmic flops of the DMMA rotation products (+ the Rayleigh-quotient GEMM below)
   if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + (refine ? 2.0 * (double)n * n * (double)L.np : 0.0);
