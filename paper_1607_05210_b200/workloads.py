@@ -91,22 +91,79 @@ def pulse_params(cols: np.ndarray, seed: int):
     return t[cols], w[cols]
 
 
-def sine_columns(d: int, cols: np.ndarray, seed: int, modes: int = 300, noise: float = 1e-8):
-    """S[:, j] = sum_{k<=300} k^-2 a_jk sin(k pi x) + noise * N(0,1), x uniform on [0,1]."""
+_SINE_COEF: dict = {}
+
+
+def _sine_coefficients(seed: int, nmax: int, modes: int) -> np.ndarray:
+    """Rows 0..nmax-1 of the seeded N(0,1) coefficient stream (row j = column j's a_j.);
+    the stream is drawn row-major, so a prefix does not depend on how many rows are drawn."""
+    have = _SINE_COEF.get((seed, modes))
+    if have is None or have.shape[0] < nmax:
+        ss = np.random.SeedSequence([int(seed), 3])
+        rng = np.random.Generator(np.random.Philox(ss))
+        have = rng.standard_normal((max(nmax, 1), modes))
+        _SINE_COEF[(seed, modes)] = have
+    return have[:nmax]
+
+
+def sine_columns(d: int, cols: np.ndarray, seed: int, noise_key: int = 0, modes: int = 300, noise: float = 1e-8):
+    """S[:, j] = sum_{k<=300} k^-2 a_jk sin(k pi x) + noise * N(0,1), x uniform on [0,1].
+    The noise of one generation unit (a 512-column slice, ``noise_key``) comes from its own
+    seeded stream, so a slice generated alone equals the same columns of the whole matrix."""
     torch = D.torch
     x = torch.linspace(0.0, 1.0, d, dtype=torch.float64, device="cuda")
     k = torch.arange(1, modes + 1, dtype=torch.float64, device="cuda")
     basis = torch.sin(math.pi * k[:, None] * x[None, :])  # (modes, d)
-    ss = np.random.SeedSequence([int(seed), 3])
-    rng = np.random.Generator(np.random.Philox(ss))
     nmax = int(cols.max()) + 1 if cols.size else 0
-    a = rng.standard_normal((nmax, modes))[cols] / (np.arange(1, modes + 1) ** 2)[None, :]
+    a = _sine_coefficients(seed, nmax, modes)[cols] / (np.arange(1, modes + 1) ** 2)[None, :]
     coef = torch.from_numpy(a).to("cuda")
     out = coef @ basis  # (cols, d)
     g = torch.Generator(device="cuda")
-    g.manual_seed(int(seed) * 7919 + int(cols[0]) if cols.size else 0)
+    g.manual_seed(int(seed) * 7919 + 104729 * int(noise_key) + 1)
     out += noise * torch.randn(out.shape, dtype=torch.float64, device="cuda", generator=g)
     return out.t()
+
+
+def _mixed_perm(seed: int, m: int) -> np.ndarray:
+    return np.random.Generator(np.random.Philox(np.random.SeedSequence([seed, 4]))).permutation(m)
+
+
+def slice_values(index: int, b: int, d: int | None = None, m: int | None = None, seed: int | None = None):
+    """Columns [block*b, block*(b+1)) of config ``index`` as a (d, block) column-major CUDA
+    tensor -- the streaming generator of the large configs (c2-c4: one slice resident at a
+    time).  ``make`` assembles the same slices, so streamed and whole-matrix runs see
+    byte-identical snapshots."""
+    cfg = CONFIGS[index]
+    d = int(d or cfg["d"])
+    m = int(m or cfg["m"])
+    seed = index if seed is None else seed
+    blk = cfg["block"]
+    cols = np.arange(b * blk, min(m, (b + 1) * blk))
+    if cfg["kind"] == "pulse":
+        return pulse_columns(d, cols, seed)
+    if cfg["kind"] == "sine":
+        return sine_columns(d, cols, seed, noise_key=b)
+    if cfg["kind"] != "mixed":
+        raise ValueError(f"config {index} is not generated by slices")
+    torch = D.torch
+    perm = _mixed_perm(seed, m)
+    is_sine = perm[cols] < m // 2
+    out = torch.empty((cols.size, d), dtype=torch.float64, device="cuda")
+    if is_sine.any():
+        out[torch.from_numpy(np.where(is_sine)[0]).cuda()] = sine_columns(d, cols[is_sine], seed, noise_key=b).t()
+    if (~is_sine).any():
+        out[torch.from_numpy(np.where(~is_sine)[0]).cuda()] = pulse_columns(d, cols[~is_sine], seed).t()
+    return out.t()
+
+
+def frobenius_norm(index: int, d: int | None = None, m: int | None = None, seed: int | None = None) -> float:
+    """||S||_F of a sliced config, one slice resident at a time (for eps* at full size)."""
+    cfg = CONFIGS[index]
+    m = int(m or cfg["m"])
+    tot = 0.0
+    for b in range((m + cfg["block"] - 1) // cfg["block"]):
+        tot += float(D.torch.linalg.vector_norm(slice_values(index, b, d, m, seed)).item()) ** 2
+    return math.sqrt(tot)
 
 
 @dataclass
@@ -140,15 +197,12 @@ def make(index: int, d: int | None = None, m: int | None = None, seed: int | Non
         vals, sig = decay_matrix(d, m, cfg["decades"], seed)
     elif cfg["kind"] == "pulse":
         vals = pulse_columns(d, np.arange(m), seed)
-    elif cfg["kind"] == "sine":
-        vals = sine_columns(d, np.arange(m), seed)
     else:
-        perm = np.random.Generator(np.random.Philox(np.random.SeedSequence([seed, 4]))).permutation(m)
-        sine_ids = np.sort(np.where(perm < m // 2)[0])
-        pulse_ids = np.sort(np.where(perm >= m // 2)[0])
+        # sine / mixed: assembled from the streaming slices (same bytes as a streamed run)
+        blk = cfg["block"]
         vals = D.torch.empty((m, d), dtype=D.torch.float64, device="cuda")
-        vals[sine_ids] = sine_columns(d, sine_ids, seed).t()
-        vals[pulse_ids] = pulse_columns(d, pulse_ids, seed).t()
+        for b in range((m + blk - 1) // blk):
+            vals[b * blk: min(m, (b + 1) * blk)] = slice_values(index, b, d, m, seed).t()
         vals = vals.t()
     fro = float(D.torch.linalg.vector_norm(vals).item())
     return Workload(index, d, m, vals, cfg["rel"] * fro, cfg["omega"], cfg["leaves"], cfg["block"], sig)
