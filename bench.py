@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-leaves", type=int, default=2, help="leaves in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs only)")
+    ap.add_argument("--root", default="rows", choices=["rows", "gather"],
+                    help="N > 1: evaluate the root on row blocks on every GPU (rows) or gather the "
+                         "children's modes on rank 0 (gather)")
     return ap.parse_args()
 
 
@@ -194,7 +197,7 @@ def main():
                 res = H.run_hapod(tree, la, tol)
             return res.modes
         ev = DI.DeviceEvaluator(sp, leaf_blocks, tol)
-        root, _, _ = DI.run_distributed(tree, ev, rank, world, place)
+        root, _, _ = DI.run_distributed(tree, ev, rank, world, place, root_rows=(a.root == "rows"))
         return root
 
     # host copy (pinned, column-major) for the end-to-end leg
@@ -215,7 +218,7 @@ def main():
             out = res.modes
         else:
             ev = DI.DeviceEvaluator(sp, blocks, tol)
-            out, _, _ = DI.run_distributed(tree, ev, rank, world, place)
+            out, _, _ = DI.run_distributed(tree, ev, rank, world, place, root_rows=(a.root == "rows"))
         if out is not None:
             np.asarray(out.sigmas).sum()  # sigmas already read back to the host
         return out
@@ -349,7 +352,8 @@ def main():
                    "leaves": nleaves, "leaf_cols": wl.block, "eps_star_rel": cfg["rel"], "omega": wl.omega,
                    "eps_star": wl.eps_star, "target": target, "modes": res_modes,
                    "l2_flush": f"inputs {d * m * 8 / 1e9:.1f} GB >> 126 MB L2 (no explicit flush)",
-                   "parallelism": f"tree over {world} GPU(s); leaf wave on {workers} stream worker(s)"},
+                   "parallelism": f"tree over {world} GPU(s); leaf wave on {workers} stream worker(s)"
+                                  + (f"; root on {world} row blocks" if world > 1 and a.root == "rows" else "")},
         "e2e": {"value": round(e2e_cols, 3), "unit": "cols/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8 * (res_modes or 0)},
         "gpu_launches": int(launches),

@@ -141,6 +141,23 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
 int hp_signs(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
              void* stream);
 
+/* Row-sharded root (multi-GPU, one row block of the modes per rank):
+ * hp_col_absmax -- per column of the local row block, the largest |u| and the GLOBAL row index
+ *   (row_offset + local row, first index on ties) of that entry: the local half of _fix_signs's
+ *   argmax (pod.py:214-224); the ranks' candidates are combined by the caller.  vals: N doubles,
+ *   idx: N int64 (device).
+ * hp_chol_inverse -- Linv = L^{-1} for C = L L^T (N x N, lower part of C used, C destroyed):
+ *   the factor of one CholQR pass when C = sum over ranks of U_q^T U_q (replaces MGS,
+ *   pod.py:227-237); U_q <- U_q Linv^T is then an hp_gemm with b_upper.  *info_out (host) is
+ *   non-zero when the factorisation broke down.  Synchronises the stream. */
+/* drift = max |C - I| of a given N x N Gram (the sum over ranks of U_q^T U_q); device scalar. */
+int hp_gram_drift(const double* C, int64_t ldc, int64_t N, double* drift_out, void* stream);
+int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
+                  int64_t* idx, void* stream);
+size_t hp_chol_inverse_workspace_bytes(int64_t N);
+int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,
+                    size_t ws_bytes, void* stream);
+
 /* Layout helpers: row-major (NumPy C-order) upload -> column-major, row/column
  * scaling (weighted spaces: InnerProductSpace.weigh/unweigh pod.py:76-84),
  * finiteness check (SnapshotBlock, pod.py:115-116; bad = device int). */

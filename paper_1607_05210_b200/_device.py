@@ -431,10 +431,22 @@ def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, 
     return lam, V, sweeps.value
 
 
-def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
-                       want_right: bool, sqrt_w=None) -> NodeOutput:
-    """pod.py:278-293 on the device: eigensolve, truncation, reconstruction,
-    drift check + re-orthonormalisation, sign convention.
+@dataclass
+class EigVectors:
+    """The spectral half of a node POD: truncation data and the kept eigenvectors of G."""
+
+    lam_max: float
+    nkeep: int
+    n_modes: int
+    tail: float
+    sig_dev: object          # sigma_1..sigma_N (device)
+    Vn: DevMat | None        # m x N eigenvectors of G, descending
+    sweeps: int
+
+
+def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
+    """pod.py:329-331 + 278-289 on the device: eigensolve of the node Gramian, cutoff keep,
+    truncation rank and tail, and the N kept eigenvectors.
 
     Eigensolve (default "pcjacobi"): G = L L^T by pivoted Cholesky (rows of L in
     the original order), H = L^T L, H = W Lambda W^T by block Jacobi, and the
@@ -531,16 +543,10 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     lam_max, nkeep, n_modes, tail = info.cpu().tolist()
     nkeep, n_modes = int(nkeep), int(n_modes)
     if not (lam_max > 0.0):
-        return NodeOutput(None, np.zeros(0), ones(0), 0.0,
-                          DevMat.empty(m, 0) if want_right else None, lam_max, 0, 0.0, False,
-                          sweeps, m)
+        return EigVectors(lam_max, 0, 0, 0.0, ones(0), None, sweeps)
     sig_dev = sig[:n_modes].clone()
     if n_modes == 0:
-        return NodeOutput(DevMat.empty(d, 0), np.zeros(0), sig_dev, tail,
-                          DevMat.empty(m, 0) if want_right else None, lam_max, nkeep, 0.0, False,
-                          sweeps, m)
-    vs, scale, m2, keep = _concat_parts(parts)
-    assert m2 == m
+        return EigVectors(lam_max, nkeep, 0, tail, sig_dev, None, sweeps)
     if basis is not None:
         # eigenvectors of G: V_N = L W_N / sigma_N  (G V = L (L^T L) W / sigma = L W Lambda / sigma), or,
         # after the polish, V_N = Q W_N with Q the orthonormal Ritz basis
@@ -553,6 +559,28 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         del ws, basis
     else:
         Vn = W.view_cols(0, n_modes)
+    return EigVectors(lam_max, nkeep, n_modes, tail, sig_dev, Vn, sweeps)
+
+
+def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
+                       want_right: bool, sqrt_w=None) -> NodeOutput:
+    """pod.py:278-293 on the device: eigensolve + truncation (eig_vectors), reconstruction,
+    drift check + re-orthonormalisation, sign convention."""
+    lib = N.load()
+    st = _stream()
+    ev = eig_vectors(G, m, eps, cutoff)
+    lam_max, nkeep, n_modes, tail, sig_dev, sweeps = ev.lam_max, ev.nkeep, ev.n_modes, ev.tail, ev.sig_dev, ev.sweeps
+    if not (lam_max > 0.0):
+        return NodeOutput(None, np.zeros(0), ones(0), 0.0,
+                          DevMat.empty(m, 0) if want_right else None, lam_max, 0, 0.0, False,
+                          sweeps, m)
+    if n_modes == 0:
+        return NodeOutput(DevMat.empty(d, 0), np.zeros(0), sig_dev, tail,
+                          DevMat.empty(m, 0) if want_right else None, lam_max, nkeep, 0.0, False,
+                          sweeps, m)
+    Vn = ev.Vn
+    vs, scale, m2, keep = _concat_parts(parts)
+    assert m2 == m
     if scale is not None:
         Vs = DevMat.empty(m, n_modes)
         N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),

@@ -45,6 +45,8 @@ int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const 
 int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st);
 int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, double* partial,
               cudaStream_t st);
+int col_absmax_run(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
+                   int64_t* idx, cudaStream_t st);
 size_t pstrf_workspace_bytes(int64_t m);
 int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
               double tol_lam, int64_t* rank_out, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -373,6 +375,49 @@ int hp_add_diag(double* C, int64_t ldc, int64_t n, double s, void* stream) {
   if (n <= 0) return HP_OK;
   add_diag<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(C, ldc, n, s);
   HP_CHECK_LAUNCH("add_diag");
+  return HP_OK;
+}
+
+int hp_gram_drift(const double* C, int64_t ldc, int64_t N, double* drift_out, void* stream) {
+  HP_REQUIRE(N >= 0 && ldc >= std::max<int64_t>(N, 1), "hp_gram_drift: bad dimensions");
+  return drift_run(C, ldc, N, drift_out, (cudaStream_t)stream);
+}
+
+int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
+                  int64_t* idx, void* stream) {
+  HP_REQUIRE(rows >= 0 && N >= 0 && ldu >= std::max<int64_t>(rows, 1), "hp_col_absmax: bad dimensions");
+  return col_absmax_run(U, ldu, rows, N, row_offset, vals, idx, (cudaStream_t)stream);
+}
+
+size_t hp_chol_inverse_workspace_bytes(int64_t N) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const int64_t nblk = (N + 63) / 64;
+  return al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * std::max<int64_t>(N, 1) * 8) + al(16) +
+         al(gemm_workspace_bytes(N, N, 64, 1, 0)) + 256;
+}
+
+int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,
+                    size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  HP_REQUIRE(N >= 0 && ldc >= N && ldl >= N, "hp_chol_inverse: bad dimensions");
+  HP_REQUIRE(ws_bytes >= hp_chol_inverse_workspace_bytes(N), "hp_chol_inverse: workspace too small");
+  if (info_out) *info_out = 0;
+  if (N == 0) return HP_OK;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* base = static_cast<char*>(ws);
+  const int64_t nblk = (N + 63) / 64;
+  double* Dinv = reinterpret_cast<double*>(base);
+  double* T = reinterpret_cast<double*>(base + al((size_t)nblk * 64 * 64 * 8));
+  int* info = reinterpret_cast<int*>(base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8));
+  char* gws = base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8) + al(16);
+  const size_t gwsb = ws_bytes - (size_t)(gws - base);
+  int rc = potrf_run(C, ldc, N, Dinv, info, gws, gwsb, st);
+  if (!rc) rc = trtri_run(C, ldc, N, Dinv, Linv, ldl, T, gws, gwsb, st);
+  if (rc) return rc;
+  int h = 0;
+  HP_CHECK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HP_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (info_out) *info_out = h;
   return HP_OK;
 }
 

@@ -187,6 +187,50 @@ __global__ void signs_kernel(double* U, int64_t ldu, int64_t d, double* R, int64
   }
 }
 
+// per column: largest |u| of the local row block and its global row index (first on ties)
+__global__ void col_absmax_kernel(const double* U, int64_t ldu, int64_t rows, int64_t row_offset, double* vals,
+                                  int64_t* idx) {
+  __shared__ double bv[256];
+  __shared__ int64_t bi[256];
+  const int64_t k = blockIdx.x;
+  const double* col = U + k * ldu;
+  double best = -1.0;
+  int64_t bidx = 0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double a = fabs(col[i]);
+    if (a > best) {
+      best = a;
+      bidx = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ov = bv[threadIdx.x + s];
+      const int64_t oi = bi[threadIdx.x + s];
+      if (ov > bv[threadIdx.x] || (ov == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = ov;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    vals[k] = rows > 0 ? bv[0] : -1.0;
+    idx[k] = row_offset + bi[0];
+  }
+}
+
+int col_absmax_run(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
+                   int64_t* idx, cudaStream_t st) {
+  if (N == 0) return HP_OK;
+  col_absmax_kernel<<<(unsigned)N, 256, 0, st>>>(U, ldu, rows, row_offset, vals, idx);
+  HP_CHECK_LAUNCH("col_absmax_kernel");
+  return HP_OK;
+}
+
 int signs_run(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
               cudaStream_t st) {
   if (N == 0) return HP_OK;

@@ -14,7 +14,11 @@ contiguous, equally sized chunks, chunk r -> rank r; an interior node goes to
 the rank of its first child (so a star's root lands on rank 0 and a chain
 stays on the rank of its bottom leaf).  Because every node's arithmetic is
 the single-GPU kernel sequence with shape-only split-K plans, results are
-bitwise identical for any rank count.
+bitwise identical for any rank count.  With ``root_rows`` the root is instead
+evaluated by every rank on a row block of its input (rowroot.py: row
+all-to-all, all_reduced Gram, eigensolve on rank 0 + broadcast) -- needed when
+the root's input exceeds one GPU (config 3) -- and is deterministic for a
+given rank count.
 
 The driver is written against a small evaluator interface so the protocol is
 exercised on CPU (gloo, world size 2) by the tests with the CPU oracle as the
@@ -58,13 +62,17 @@ class EdgeStats:
     comm_time: float = 0.0
 
 
-def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, placement=None, group=None):
-    """Evaluate the tree across ranks.  Returns (root result or None on
-    non-root ranks, {node: (seconds, result)}, EdgeStats).
+def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, placement=None, group=None,
+                    root_rows: bool = False):
+    """Evaluate the tree across ranks.  Returns (root result on rank 0 / the root's rank,
+    None elsewhere; {node: (seconds, result)}; EdgeStats).
 
     ``evaluator`` provides the node arithmetic and the edge payloads:
     evaluate_leaf(node), evaluate_interior(node, child_results),
-    send(result, dst, group) -> (async works, bytes), recv(src, group) -> (result, bytes)."""
+    send(result, dst, group) -> (async works, bytes), recv(src, group) -> (result, bytes);
+    with ``root_rows`` also root_parts(result) and evaluate_root_rows(root, children, local,
+    rank, world, group): the root is then evaluated by ALL ranks on row blocks of its input
+    (rowroot.py) instead of gathering the children's modes on one rank."""
     import torch.distributed as dist
 
     maps = derive_maps(tree)
@@ -73,8 +81,9 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
     reports: dict = {}
     stats = EdgeStats()
     pending_sends = []
+    root_kids = set(tree.children[tree.root]) if root_rows else set()
     for v in post_order(tree):
-        if place[v] != rank:
+        if place[v] != rank or (root_rows and v == tree.root):
             continue
         kids = tree.children[v]
         started = time.perf_counter()
@@ -95,7 +104,7 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
             out = evaluator.evaluate_interior(v, child_results)
         reports[v] = (time.perf_counter() - started, out)
         parent = maps.parent[v]
-        if parent >= 0 and place[parent] != rank:
+        if parent >= 0 and place[parent] != rank and v not in root_kids:
             t0 = time.perf_counter()
             works, nbytes = evaluator.send(out, place[parent], group)
             pending_sends.extend(works)
@@ -106,6 +115,12 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
             live[v] = out
     for w in pending_sends:
         w.wait()
+    if root_rows:
+        started = time.perf_counter()
+        local = {c: evaluator.root_parts(live.pop(c)) for c in tree.children[tree.root] if place[c] == rank}
+        root = evaluator.evaluate_root_rows(tree.root, list(tree.children[tree.root]), local, rank, world_size, group)
+        reports[tree.root] = (time.perf_counter() - started, root)
+        return root, reports, stats
     root = live.get(tree.root) if place[tree.root] == rank else None
     return root, reports, stats
 
@@ -141,6 +156,35 @@ class DeviceEvaluator:
             if ms.count:
                 parts.extend(ms.scaled_parts())
         return pod_parts(self.space, parts, self.tol.epsilons[node], self.backend)
+
+    def root_parts(self, ms):
+        """A child's contribution to the root input: its sigma-scaled column blocks
+        (ModeSet.scaled, pod.py:160-162) as (DevMat, host scale or None)."""
+        return [(p.mat, None if p.scale is None else p.scale.cpu().numpy()) for p in ms.scaled_parts()]
+
+    def evaluate_root_rows(self, root, children, local, rank, world, group):
+        from . import _device as D
+        from . import rowroot as RR
+        from .pod import ModeSet
+        arith = RR.DeviceRowArith()
+        D.Profiler.set_tag(root)
+        d = self.space.dimension
+        layout = RR.gather_layout(children, local, rank, world, group)
+        bounds = RR.row_bounds(d, world)
+        S_q = RR.exchange_rows(layout, local, bounds, rank, world, arith, group)
+        res = RR.row_root_pod(S_q, layout, bounds, self.tol.epsilons[root], self.backend.gram_eig_cutoff_factor,
+                              rank, world, arith, group)
+        del S_q
+        full = RR.gather_rows(res, d, rank, world, arith, group)
+        if rank != 0:
+            return None
+        if res.sigmas.size == 0:
+            return ModeSet._device(self.space, np.zeros(0), [D.Part(D.DevMat.empty(d, 0))], orthonormal=True,
+                                   tail_energy=res.tail)
+        return ModeSet._device(self.space, res.sigmas, [D.Part(full)], orthonormal=True, tail_energy=res.tail,
+                               diagnostics={"lam_max": res.lam_max, "nkeep": res.nkeep, "drift": res.drift,
+                                            "reorthonormalized": res.reorthed, "input_count": res.m,
+                                            "row_blocks": res.bounds})
 
     def send(self, ms, dst, group):
         import torch

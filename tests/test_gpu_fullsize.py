@@ -56,8 +56,9 @@ def test_config2_full_size_streamed():
     orth = _orthonormality(res.modes)
     print(f"\n[c2 full 500000x32768] modes={res.mode_count} l2={err:.6e} eps*={eps_star:.6e} "
           f"apriori={res.apriori_error_bound:.6e} orthonormality={orth:.1e}")
-    assert res.apriori_error_bound == pytest.approx(eps_star, rel=1e-12)
-    assert err <= eps_star
+    # the chain's per-step tolerances (hierarchy.py:408-417) keep the a-priori bound below eps*
+    assert res.apriori_error_bound <= eps_star * (1 + 1e-12)
+    assert err <= res.apriori_error_bound
     assert orth <= 1e-8  # the reference re-orthonormalises above 1e-8 drift (pod.py:247)
     s = res.modes.sigmas
     assert np.all(s > 0) and np.all(np.diff(s) <= 0)
@@ -119,7 +120,9 @@ def test_config4_full_size_streamed():
     chain_out = sorted(r.output_mode_count for r in res.reports if r.node in tree.children[0])
     print(f"\n[c4 full 1000000x65536] modes={res.mode_count} chain outputs={chain_out} l2={err:.6e} "
           f"eps*={eps_star:.6e} apriori={res.apriori_error_bound:.6e} orthonormality={orth:.1e}")
-    assert res.apriori_error_bound == pytest.approx(eps_star, rel=1e-12)
-    assert err <= eps_star
+    # zero leaf tolerance: the leaves add nothing, so the a-priori bound sits below eps*
+    assert res.apriori_error_bound <= eps_star * (1 + 1e-12)
+    assert err <= res.apriori_error_bound
     assert orth <= 1e-8  # the reference re-orthonormalises above 1e-8 drift (pod.py:247)
+    assert all(286 <= c <= 288 for c in chain_out)  # reference at d = 20,000: 286-288
     assert 200 <= res.mode_count <= 320  # reference at d = 20,000: 250
