@@ -155,10 +155,6 @@ int hp_gram_drift(const double* C, int64_t ldc, int64_t N, double* drift_out, vo
 int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
                   int64_t* idx, void* stream);
 size_t hp_chol_inverse_workspace_bytes(int64_t N);
-/* Cholesky C = L L^T in place (lower = L, strict upper = 0); *info_out (host) non-zero on
- * breakdown.  Used for one LR step of the eigensolver: H = L L^T -> H2 = L^T L (same
- * eigenvalues, more diagonal, fewer Jacobi sweeps).  Workspace: hp_chol_inverse_workspace_bytes. */
-int hp_potrf(double* C, int64_t ldc, int64_t N, int* info_out, void* ws, size_t ws_bytes, void* stream);
 int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,
                     size_t ws_bytes, void* stream);
 

@@ -52,9 +52,6 @@ POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
 POLISH_TOL_ANGLE = float(_os.environ.get("HP_EIG_POLISH_TOL_ANGLE", "1e-14"))
 # absolute trigger of the preconditioned (H = L^T L) phase; the polish carries the final accuracy
 PC_TOL_ABS = float(_os.environ.get("HP_PC_TOL_ABS", str(16 * 2.0 ** -52)))
-# one Cholesky LR step on H before the Jacobi phase (orders >= LR_MIN)
-LR_STEP = _os.environ.get("HP_LR_STEP", "1") != "0"
-LR_MIN = int(_os.environ.get("HP_LR_MIN", "128"))
 
 
 class Profiler:
@@ -480,27 +477,6 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
                 N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
                         "H = L^T L")
             del ws
-        # One LR step (Cholesky H = Lc Lc^T, H2 = Lc^T Lc): the same eigenvalues, the off-diagonal
-        # mass of the graded H pushed further towards the diagonal -- fewer Jacobi sweeps (NumPy
-        # simulation at n = 1024: 9 -> 7 sweeps, a quarter of the pair work).  Eigenvectors map back
-        # as W = Lc W2 Lambda^{-1/2}.  Skipped if the Cholesky breaks down.
-        Lc = None
-        if POLISH and LR_STEP and r >= LR_MIN:
-            Lc = DevMat.empty(r, r)
-            info_c = ctypes.c_int(0)
-            ws = _ws(lib.hp_chol_inverse_workspace_bytes(r))
-            with _phase("lr_step", float(r) ** 3 / 3.0 + float(r) * r * (r + 1)):
-                N.check(lib.hp_scale(H.ptr, H.ld, r, r, None, None, None, Lc.ptr, Lc.ld, st), "copy H")
-                N.check(lib.hp_potrf(Lc.ptr, Lc.ld, r, ctypes.byref(info_c), ws.data_ptr(), ws.numel(), st),
-                        "LR step Cholesky")
-                if info_c.value == 0:
-                    wg = _ws(lib.hp_gram_workspace_bytes(r, r))
-                    N.check(lib.hp_gram(Lc.vecset(), r, r, None, H.ptr, H.ld, wg.data_ptr(), wg.numel(), st),
-                            "H2 = Lc^T Lc")
-                    del wg
-                else:
-                    Lc = None
-            del ws
         # with the polish, H's eigenvalues only select K and scale Q0: no Rayleigh refinement
         lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS if POLISH else None, refine=not POLISH)
         nev = r
@@ -512,15 +488,6 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
             N.check(lib.hp_truncate(lam.data_ptr(), r, 0.0, float(cutoff) * POLISH_FACTOR, m, sig_h.data_ptr(),
                                     info_h.data_ptr(), st), "polish count")
             lam_max_h, K = float(info_h[0].item()), int(info_h[1].item())
-            if K and Lc is not None:
-                # eigenvectors of H from those of H2: W_K = Lc W2_K / sigma_K
-                WK = DevMat.empty(r, K)
-                ws = _ws(lib.hp_gemm_workspace_bytes(r, K, r, 0, 0))
-                with _phase("lr_step", 2.0 * r * r * K):
-                    N.check(lib.hp_gemm(0, 1, r, K, r, Lc.vecset(), W.vecset(), 1.0, 0.0, WK.ptr, WK.ld, None, None,
-                                        sig_h.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "W = Lc W2 / sigma")
-                W = WK
-                del ws, Lc
             if K:
                 # Q0 = L W_K Lambda_K^{-1/2}: approximate eigenvectors of G from the preconditioned solve.
                 # One subspace-iteration step X = G Q0 Lambda_K^{-1} damps the components along

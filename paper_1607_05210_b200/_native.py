@@ -64,7 +64,6 @@ _SIGNATURES = {
     "hp_col_absmax": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "hp_chol_inverse_workspace_bytes": (c_size, [c_i64]),
     "hp_chol_inverse": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_size, c_vp]),
-    "hp_potrf": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_size, c_vp]),
     "hp_sumsq_workspace_bytes": (c_size, []),
     "hp_sumsq": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_size, c_vp]),
 }

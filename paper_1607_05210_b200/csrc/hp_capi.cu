@@ -421,28 +421,6 @@ int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl
   return HP_OK;
 }
 
-int hp_potrf(double* C, int64_t ldc, int64_t N, int* info_out, void* ws, size_t ws_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  HP_REQUIRE(N >= 0 && ldc >= N, "hp_potrf: bad dimensions");
-  HP_REQUIRE(ws_bytes >= hp_chol_inverse_workspace_bytes(N), "hp_potrf: workspace too small");
-  if (info_out) *info_out = 0;
-  if (N == 0) return HP_OK;
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  char* base = static_cast<char*>(ws);
-  const int64_t nblk = (N + 63) / 64;
-  double* Dinv = reinterpret_cast<double*>(base);
-  int* info = reinterpret_cast<int*>(base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8));
-  char* gws = base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8) + al(16);
-  const size_t gwsb = ws_bytes - (size_t)(gws - base);
-  int rc = potrf_run(C, ldc, N, Dinv, info, gws, gwsb, st);
-  if (rc) return rc;
-  int h = 0;
-  HP_CHECK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));
-  HP_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (info_out) *info_out = h;
-  return HP_OK;
-}
-
 size_t hp_sumsq_workspace_bytes(void) { return 1024 * sizeof(double); }
 
 int hp_sumsq(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, void* ws, size_t ws_bytes,
