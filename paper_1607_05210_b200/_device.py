@@ -370,7 +370,7 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     return G, total, keep
 
 
-BJORCK_MAX_DRIFT = 0.05   # Newton-Schulz converges quadratically from here (3 steps to ~u)
+BJORCK_MAX_DRIFT = float(_os.environ.get("HP_BJORCK_MAX_DRIFT", "0.05"))  # Newton-Schulz: quadratic from here
 
 
 def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:

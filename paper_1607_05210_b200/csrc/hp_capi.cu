@@ -17,6 +17,12 @@ void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_rel
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
+char* pinned_scratch() {
+  thread_local char* buf = nullptr;
+  if (!buf && cudaMallocHost(&buf, 256) != cudaSuccess) buf = nullptr;
+  return buf;
+}
+
 int num_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -77,7 +83,9 @@ static ReorthoLayout reortho_layout(int64_t d, int64_t N, int64_t ldx) {
   L.off_info = o;
   o = al(o + 16);
   L.off_gemm = o;
-  size_t g = std::max(gemm_workspace_bytes(N, N, d, 1, 0), gemm_workspace_bytes(N, N, 64, 1, 0));
+  // the triangular inverse's row-block products (64 x r0 x r0) need split-K to fill the chip
+  size_t g = std::max(std::max(gemm_workspace_bytes(N, N, d, 1, 0), gemm_workspace_bytes(N, N, 64, 1, 0)),
+                      gemm_workspace_bytes(64, N, N, 0, 0));
   o = al(o + g);
   L.total = o;
   return L;
@@ -272,10 +280,10 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
   const int64_t ldn = (N + 1) & ~int64_t(1);
   void* gws = base + L.off_gemm;
   const size_t gwsb = ws_bytes - L.off_gemm;
-  int* hinfo = nullptr;
-  HP_CHECK_CUDA(cudaMallocHost(&hinfo, 2 * sizeof(int)));
-  double* htrace = nullptr;
-  HP_CHECK_CUDA(cudaMallocHost(&htrace, sizeof(double)));
+  char* pin = pinned_scratch();
+  HP_REQUIRE(pin != nullptr, "hp_reorthonormalize: pinned host scratch unavailable");
+  int* hinfo = reinterpret_cast<int*>(pin + 64);
+  double* htrace = reinterpret_cast<double*>(pin + 80);
   int rc = HP_OK;
   int passes = 0;
   // keep a copy of C in case the first factorisation fails
@@ -321,8 +329,6 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
         rc = HP_ECUDA;
       }
     }
-    cudaFreeHost(hinfo);
-    cudaFreeHost(htrace);
     return rc;
   }
   // second pass: X -> U
@@ -339,8 +345,6 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
       rc = HP_ELINALG;
     }
   }
-  cudaFreeHost(hinfo);
-  cudaFreeHost(htrace);
   if (passes_out) *passes_out = passes;
   return rc;
 }
@@ -393,7 +397,7 @@ size_t hp_chol_inverse_workspace_bytes(int64_t N) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const int64_t nblk = (N + 63) / 64;
   return al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * std::max<int64_t>(N, 1) * 8) + al(16) +
-         al(gemm_workspace_bytes(N, N, 64, 1, 0)) + 256;
+         al(std::max(gemm_workspace_bytes(N, N, 64, 1, 0), gemm_workspace_bytes(64, N, N, 0, 0))) + 256;
 }
 
 int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,

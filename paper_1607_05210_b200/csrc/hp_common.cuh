@@ -129,5 +129,9 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int num_sms();
+// Pinned host scratch of the calling host thread (allocated once, never freed per call: a
+// cudaFreeHost per call would synchronise the whole device and serialise concurrent node
+// streams).  Slots: [0, 64) Jacobi sweep counters, [64, 128) re-orthonormalisation flags.
+char* pinned_scratch();
 
 }  // namespace hp

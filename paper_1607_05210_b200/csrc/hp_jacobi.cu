@@ -700,8 +700,8 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   HP_CHECK_CUDA(cudaGetDevice(&dev));
   HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
 
-  char* host_buf = nullptr;
-  HP_CHECK_CUDA(cudaMallocHost(&host_buf, 32));
+  char* host_buf = pinned_scratch();
+  HP_REQUIRE(host_buf != nullptr, "syev: pinned host scratch unavailable");
   HP_CHECK_CUDA(cudaMemsetAsync(p.mm_count, 0, 8, st));
   int status = HP_ELINALG;
   int sweep = 0;
@@ -760,7 +760,6 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-      cudaFreeHost(host_buf);
       set_error(std::string("syev sweep: ") + cudaGetErrorString(e));
       return HP_ECUDA;
     }
@@ -782,7 +781,6 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     }
     prev_off = off;
   }
-  cudaFreeHost(host_buf);
   if (sweeps_out) *sweeps_out = sweep + (status == HP_OK ? 1 : 0);
   // algorithmic flops of the DMMA rotation products (+ the Rayleigh-quotient GEMM below)
   if (flops_out) *flops_out = (double)mm_total * 2.0 * PS * PS * PS + (refine ? 2.0 * (double)n * n * (double)L.np : 0.0);
