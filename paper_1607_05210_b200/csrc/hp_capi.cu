@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // extern "C" boundary of libhapod_b200.so (declared in include/hapod_b200.h).
 // Plain pointers and sizes only; every entry returns an hp status code and
 // leaves a thread-local message for hp_last_error().
@@ -42,9 +44,9 @@ int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
 int signs_run(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ldr, int64_t mr, double* sign_out,
               cudaStream_t st);
-int potrf_run(double* A, int64_t lda, int64_t n, double* Dinv, int* info, void* ws, size_t ws_bytes, cudaStream_t st);
-int trtri_run(const double* L, int64_t ldl, int64_t n, const double* Dinv, double* Linv, int64_t ldi, double* T,
-              void* ws, size_t ws_bytes, cudaStream_t st);
+int64_t chol_t_cols(int64_t n);
+int chol_inv_run(double* C, int64_t ldc, int64_t n, double* Linv, int64_t ldi, double* T, int* info, void* ws,
+                 size_t ws_bytes, cudaStream_t st);
 int transpose_run(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ldd, cudaStream_t st);
 int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* rs, const double* rd,
               const double* cs, double* dst, int64_t ldd, cudaStream_t st);
@@ -60,15 +62,17 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
 static inline VecSet vs(const hp_vecset& v) { return VecSet{v.base, v.ld, v.table}; }
 
 // ---------------------------------------------------------------- re-orthonormalisation
+// split-K partials of any GEMM the engine plans (splits x tiles <= 2 waves of 148 SMs)
+static constexpr size_t kSplitKMax = (size_t)2 * 148 * 128 * 128 * 8;
+
 struct ReorthoLayout {
-  size_t off_X, off_A, off_Linv, off_Dinv, off_T, off_info, off_gemm, total;
+  size_t off_X, off_A, off_Linv, off_T, off_info, off_gemm, total;
 };
 
 static ReorthoLayout reortho_layout(int64_t d, int64_t N, int64_t ldx) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   ReorthoLayout L;
   size_t o = 0;
-  const int64_t nblk = (N + 63) / 64;
   const int64_t ldn = (N + 1) & ~int64_t(1);
   L.off_X = o;
   o = al(o + (size_t)ldx * N * 8);
@@ -76,16 +80,13 @@ static ReorthoLayout reortho_layout(int64_t d, int64_t N, int64_t ldx) {
   o = al(o + (size_t)ldn * N * 8);
   L.off_Linv = o;
   o = al(o + (size_t)ldn * N * 8);
-  L.off_Dinv = o;
-  o = al(o + (size_t)nblk * 64 * 64 * 8);
   L.off_T = o;
-  o = al(o + (size_t)64 * std::max<int64_t>(N, 1) * 8);
+  o = al(o + (size_t)ldn * chol_t_cols(N) * 8);
   L.off_info = o;
   o = al(o + 16);
   L.off_gemm = o;
-  // the triangular inverse's row-block products (64 x r0 x r0) need split-K to fill the chip
-  size_t g = std::max(std::max(gemm_workspace_bytes(N, N, d, 1, 0), gemm_workspace_bytes(N, N, 64, 1, 0)),
-                      gemm_workspace_bytes(64, N, N, 0, 0));
+  // the Cholesky/inverse recursion's mid-size products may split K to fill the chip
+  size_t g = std::max(gemm_workspace_bytes(N, N, d, 1, 0), kSplitKMax);
   o = al(o + g);
   L.total = o;
   return L;
@@ -96,17 +97,14 @@ static int cholqr_pass(const double* X, int64_t ldx, int64_t d, int64_t N, doubl
                        int64_t ldy, const ReorthoLayout& L, char* base, size_t ws_bytes, cudaStream_t st,
                        int* host_info) {
   double* Linv = reinterpret_cast<double*>(base + L.off_Linv);
-  double* Dinv = reinterpret_cast<double*>(base + L.off_Dinv);
   double* T = reinterpret_cast<double*>(base + L.off_T);
   int* info = reinterpret_cast<int*>(base + L.off_info);
   void* gws = base + L.off_gemm;
   const size_t gwsb = ws_bytes - L.off_gemm;
   const int64_t ldn = (N + 1) & ~int64_t(1);
-  int rc = potrf_run(C, ldc, N, Dinv, info, gws, gwsb, st);
+  int rc = chol_inv_run(C, ldc, N, Linv, ldn, T, info, gws, gwsb, st);
   if (rc) return rc;
   HP_CHECK_CUDA(cudaMemcpyAsync(host_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
-  rc = trtri_run(C, ldc, N, Dinv, Linv, ldn, T, gws, gwsb, st);
-  if (rc) return rc;
   // Y = X * Linv^T : B(k, n) = Linv(n, k) -> N-major operand (vector k = column k of Linv), upper triangular
   VecSet a{X, ldx, nullptr};
   VecSet b{Linv, ldn, nullptr};
@@ -393,11 +391,13 @@ int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t
   return col_absmax_run(U, ldu, rows, N, row_offset, vals, idx, (cudaStream_t)stream);
 }
 
+static size_t tbytes(int64_t N) {
+  return (size_t)((std::max<int64_t>(N, 1) + 1) & ~int64_t(1)) * chol_t_cols(N) * 8;
+}
+
 size_t hp_chol_inverse_workspace_bytes(int64_t N) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const int64_t nblk = (N + 63) / 64;
-  return al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * std::max<int64_t>(N, 1) * 8) + al(16) +
-         al(std::max(gemm_workspace_bytes(N, N, 64, 1, 0), gemm_workspace_bytes(64, N, N, 0, 0))) + 256;
+  return al(tbytes(N)) + al(16) + al(kSplitKMax) + 256;
 }
 
 int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,
@@ -409,14 +409,26 @@ int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl
   if (N == 0) return HP_OK;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* base = static_cast<char*>(ws);
-  const int64_t nblk = (N + 63) / 64;
-  double* Dinv = reinterpret_cast<double*>(base);
-  double* T = reinterpret_cast<double*>(base + al((size_t)nblk * 64 * 64 * 8));
-  int* info = reinterpret_cast<int*>(base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8));
-  char* gws = base + al((size_t)nblk * 64 * 64 * 8) + al((size_t)64 * N * 8) + al(16);
+  double* T = reinterpret_cast<double*>(base);
+  int* info = reinterpret_cast<int*>(base + al(tbytes(N)));
+  char* gws = base + al(tbytes(N)) + al(16);
   const size_t gwsb = ws_bytes - (size_t)(gws - base);
-  int rc = potrf_run(C, ldc, N, Dinv, info, gws, gwsb, st);
-  if (!rc) rc = trtri_run(C, ldc, N, Dinv, Linv, ldl, T, gws, gwsb, st);
+  static const bool trace = getenv("HP_TRACE_CHOL") != nullptr;
+  cudaEvent_t ev[3];
+  if (trace)
+    for (auto& e : ev) cudaEventCreate(&e);
+  if (trace) cudaEventRecord(ev[0], st);
+  int rc = chol_inv_run(C, ldc, N, Linv, ldl, T, info, gws, gwsb, st);
+  if (trace) cudaEventRecord(ev[1], st);
+  if (trace) {
+    cudaEventRecord(ev[2], st);
+    cudaEventSynchronize(ev[2]);
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    fprintf(stderr, "[hp_chol_inverse n=%lld] chol_inv %.2f ms (+%.2f)\n", (long long)N, a, b);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   if (rc) return rc;
   int h = 0;
   HP_CHECK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));

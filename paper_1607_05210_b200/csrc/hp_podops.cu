@@ -16,6 +16,8 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
              double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
              const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* rs, const double* rd,
+              const double* cs, double* dst, int64_t ldd, cudaStream_t st);
 
 // ------------------------------------------------------------------ K3 truncation
 // info[0] = lam_max, info[1] = nkeep, info[2] = N, info[3] = tail_energy
@@ -242,9 +244,13 @@ int signs_run(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t l
 // ------------------------------------------------------------------ Cholesky (CholQR)
 constexpr int CB = 64;
 
-// Factor the kb x kb diagonal block at A[k0,k0] (lower, in place), write
-// Dinv = (L_kk^{-1})^T col-major (ld CB) and flag a non-positive pivot.
-__global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_t k0, int kb, double* Dinv, int* info) {
+// Factor the kb x kb diagonal block at A[k0,k0] (lower, in place), write its inverse into
+// Linv[k0.., k0..] (lower) and flag a non-positive pivot.
+// Right-looking and fused: step j takes the pivot, scales column j of L and row j of
+// X = L^{-1} (X solves L X = I; R holds the running right-hand side), then applies the rank-1
+// updates to the trailing block of A and to R -- 64 steps of 3 barriers, no serial loops.
+__global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_t k0, int kb, double* Linv, int64_t ldi,
+                                                   int* info) {
   extern __shared__ double pd_smem[];
   double (*L)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(pd_smem);
   double (*X)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(pd_smem + CB * (CB + 1));
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_
   for (int e = tid; e < CB * CB; e += 256) {
     const int j = e / CB, i = e % CB;
     L[i][j] = (i < kb && j < kb && i >= j) ? A[(k0 + j) * lda + k0 + i] : 0.0;
-    X[i][j] = 0.0;
+    X[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   for (int j = 0; j < kb; ++j) {
@@ -268,114 +274,96 @@ __global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_
       }
     }
     __syncthreads();
-    const double piv = L[j][j];
-    for (int i = j + 1 + tid; i < kb; i += 256) L[i][j] /= piv;
+    const double rpiv = 1.0 / L[j][j];
+    if (tid < CB) {
+      if (tid > j && tid < kb) L[tid][j] *= rpiv;       // column j of L
+    } else if (tid - CB <= j) {
+      X[j][tid - CB] *= rpiv;                           // row j of L^{-1}: X[j][c] = R[j][c] / L[j][j]
+    }
     __syncthreads();
-    const int rem = kb - j - 1;
-    for (int e = tid; e < rem * rem; e += 256) {
-      const int ii = j + 1 + e / rem, kk = j + 1 + e % rem;
-      if (kk <= ii) L[ii][kk] -= L[ii][j] * L[kk][j];
+    // trailing A -= l_j l_j^T (lower part) and R[i][c] -= L[i][j] X[j][c] (i > j, c <= j):
+    // thread = (column c, row phase), no index division
+    {
+      const int c = tid & (CB - 1);
+      const double xjc = X[j][c], lcj = L[c][j];
+      for (int ii = j + 1 + (tid >> 6); ii < kb; ii += 256 / CB) {
+        const double lij = L[ii][j];
+        if (c <= j)
+          X[ii][c] -= lij * xjc;
+        else if (c <= ii)
+          L[ii][c] -= lij * lcj;
+      }
     }
     __syncthreads();
   }
-  // X = L^{-1} by forward substitution, one column per thread
-  if (tid < kb) {
-    const int c = tid;
-    X[c][c] = 1.0 / L[c][c];
-    for (int i = c + 1; i < kb; ++i) {
-      double s = 0.0;
-      for (int q = c; q < i; ++q) s += L[i][q] * X[q][c];
-      X[i][c] = -s / L[i][i];
-    }
-  }
-  __syncthreads();
   for (int e = tid; e < kb * kb; e += 256) {
     const int j = e / kb, i = e % kb;
     A[(k0 + j) * lda + k0 + i] = (i >= j) ? L[i][j] : 0.0;
-    // Dinv(k', n) = X(n, k') stored col-major with ld CB: Dinv[n*CB + k'] ... i.e. element (row i, col j) = X(j, i)
-    Dinv[j * CB + i] = X[j][i];
+    Linv[(k0 + j) * ldi + k0 + i] = (i >= j) ? X[i][j] : 0.0;
   }
   if (tid == 0 && bad) atomicOr(info, 1);
 }
 
-// Lower Cholesky of the n x n symmetric matrix A (lower part used, whole matrix
-// overwritten: lower = L, strict upper = 0).  Dinv receives the transposed
-// inverses of the diagonal blocks (nblk x CB x CB).
-int potrf_run(double* A, int64_t lda, int64_t n, double* Dinv, int* info, void* ws, size_t ws_bytes, cudaStream_t st) {
-  HP_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
-  const int pd_smem = 2 * CB * (CB + 1) * 8;
-  static bool configured = false;
-  if (!configured) {
-    HP_CHECK_CUDA(cudaFuncSetAttribute(potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem));
-    configured = true;
-  }
-  for (int64_t k0 = 0; k0 < n; k0 += CB) {
-    const int kb = (int)std::min<int64_t>(CB, n - k0);
-    double* Dk = Dinv + (k0 / CB) * CB * CB;
-    potrf_diag<<<1, 256, pd_smem, st>>>(A, lda, k0, kb, Dk, info);
+// Cholesky factor AND its inverse, C = L L^T, Linv = L^{-1}, by recursive halving
+// (C = [[C11, .], [C21, C22]]):
+//   L11, X11 = chol_inv(C11);  L21 = C21 X11^T;  C22 -= L21 L21^T;  L22, X22 = chol_inv(C22);
+//   X21 = -X22 (L21 X11)
+// The 64 x 64 leaves are potrf_diag; everything else is DMMA GEMMs whose big instances are
+// full-size GEMM shapes (the former block-column loop launched 3 small kernels per 64 columns
+// and re-wrote the whole trailing matrix each time).  C's lower part is consumed.  T: scratch
+// of ldt x chol_t_cols(n) doubles.
+static int chol_inv_rec(double* A, int64_t lda, int64_t o, int64_t n, double* Linv, int64_t ldi, double* T,
+                        int64_t ldt, int* info, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= CB) {
+    static bool configured = false;
+    const int pd_smem = 2 * CB * (CB + 1) * 8;
+    if (!configured) {
+      HP_CHECK_CUDA(cudaFuncSetAttribute(potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem));
+      configured = true;
+    }
+    potrf_diag<<<1, 256, pd_smem, st>>>(A, lda, o, (int)n, Linv, ldi, info);
     HP_CHECK_LAUNCH("potrf_diag");
-    const int64_t rest = n - k0 - kb;
-    if (rest <= 0) continue;
-    double* P = A + k0 * lda + k0 + kb;  // panel rows k0+kb.., cols k0..k0+kb
-    // P <- P * L_kk^{-T}   (B(k', n) = Linv(n, k') = Dk[k' + n*CB] ... K-major columns of Dk^T)
-    VecSet a{P, lda, nullptr};
-    VecSet b{Dk, CB, nullptr};
-    // B(k', n) must equal (L^{-T})(k', n) = Linv(n, k') = X[n][k'] = Dk[k' * CB + n]
-    // as a K-major operand vector n is contiguous along k': Dk stored with element
-    // (i=k', j=n) at j*CB + i holds X[j][i]?  Dk[j*CB+i] = X[j][i] = Linv(j, i): vector n=j
-    // contiguous along k'=i gives Linv(n, k') -- exactly L^{-T}(k', n).
-    int rc = gemm_run(false, true, rest, kb, kb, a, b, (lda % 2 == 0), 1.0, 0.0, P, lda, nullptr, nullptr, nullptr,
-                      0, 0, nullptr, 0, st);
-    if (rc) return rc;
-    // trailing update A22 -= P P^T (symmetric)
-    double* A22 = A + (k0 + kb) * lda + k0 + kb;
-    VecSet pa{P, lda, nullptr};  // A operand: M-major, vector k' = column of P
-    VecSet pb{P, lda, nullptr};  // B operand N-major: B(k', n) = P(n, k'), vector k' contiguous along n
-    rc = gemm_run(false, false, rest, rest, kb, pa, pb, (lda % 2 == 0), -1.0, 1.0, A22, lda, nullptr, nullptr,
-                  nullptr, 1, 0, ws, ws_bytes, st);
-    if (rc) return rc;
+    return HP_OK;
   }
-  return HP_OK;
+  int64_t h = ceil_div(n / 2, CB) * CB;
+  if (h >= n) h = n - CB;
+  const int64_t n2 = n - h;
+  const bool al = (lda % 2 == 0) && (ldi % 2 == 0) && (ldt % 2 == 0) && (o % 2 == 0) && (h % 2 == 0);
+  int rc = chol_inv_rec(A, lda, o, h, Linv, ldi, T, ldt, info, ws, ws_bytes, st);
+  if (rc) return rc;
+  double* X11 = Linv + o * ldi + o;
+  double* X21 = Linv + o * ldi + o + h;
+  double* X22 = Linv + (o + h) * ldi + o + h;
+  double* C21 = A + o * lda + o + h;
+  double* C22 = A + (o + h) * lda + o + h;
+  // T = L21 = C21 X11^T   (B(k, j) = X11(j, k): N-major operand)
+  rc = gemm_run(false, false, n2, h, h, VecSet{C21, lda, nullptr}, VecSet{X11, ldi, nullptr}, al, 1.0, 0.0, T, ldt,
+                nullptr, nullptr, nullptr, 0, 0, ws, ws_bytes, st);
+  // C22 -= L21 L21^T
+  if (!rc)
+    rc = gemm_run(false, false, n2, n2, h, VecSet{T, ldt, nullptr}, VecSet{T, ldt, nullptr}, al, -1.0, 1.0, C22, lda,
+                  nullptr, nullptr, nullptr, 1, 0, ws, ws_bytes, st);
+  // X21 <- L21 X11 (parked in its final place), then T is free for the recursion
+  if (!rc)
+    rc = gemm_run(false, true, n2, h, h, VecSet{T, ldt, nullptr}, VecSet{X11, ldi, nullptr}, al, 1.0, 0.0, X21, ldi,
+                  nullptr, nullptr, nullptr, 0, 0, ws, ws_bytes, st);
+  if (!rc) rc = chol_inv_rec(A, lda, o + h, n2, Linv, ldi, T, ldt, info, ws, ws_bytes, st);
+  // X21 = -X22 (L21 X11)
+  if (!rc)
+    rc = gemm_run(false, true, n2, h, n2, VecSet{X22, ldi, nullptr}, VecSet{X21, ldi, nullptr}, al, -1.0, 0.0, T, ldt,
+                  nullptr, nullptr, nullptr, 0, 0, ws, ws_bytes, st);
+  if (!rc) rc = scale_run(T, ldt, n2, h, nullptr, nullptr, nullptr, X21, ldi, st);
+  return rc;
 }
 
-__global__ void copy_diag_inverse(const double* Dinv, int64_t n, double* Linv, int64_t ld) {
-  // Linv(i, j) for the diagonal blocks = X(i, j) = Dinv_blk[i_l*CB + j_l]... (Dinv[j*CB+i] = X[j][i])
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nblk = ceil_div(n, CB);
-  if (e >= nblk * CB * CB) return;
-  const int64_t blk = e / (CB * CB);
-  const int r = (int)(e % (CB * CB));
-  const int jl = r / CB, il = r % CB;  // element stored at Dinv[jl*CB+il] = X[jl][il]
-  const int64_t gi = blk * CB + jl, gj = blk * CB + il;  // X row jl, col il
-  if (gi < n && gj < n) Linv[gj * ld + gi] = Dinv[e];
-}
+int64_t chol_t_cols(int64_t n) { return std::max<int64_t>(ceil_div(std::max<int64_t>(n, 1) / 2, CB) * CB, CB); }
 
-// Linv = L^{-1} (lower), blocked by block rows:
-//   T = L[i, 0:i] Linv[0:i, 0:i];   Linv[i, 0:i] = -L_ii^{-1} T
-int trtri_run(const double* L, int64_t ldl, int64_t n, const double* Dinv, double* Linv, int64_t ldi, double* T,
-              void* ws, size_t ws_bytes, cudaStream_t st) {
+int chol_inv_run(double* C, int64_t ldc, int64_t n, double* Linv, int64_t ldi, double* T, int* info, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  HP_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  if (n == 0) return HP_OK;
   HP_CHECK_CUDA(cudaMemset2DAsync(Linv, ldi * 8, 0, n * 8, n, st));
-  const int64_t nblk = ceil_div(n, CB);
-  copy_diag_inverse<<<(unsigned)ceil_div(nblk * CB * CB, 256), 256, 0, st>>>(Dinv, n, Linv, ldi);
-  HP_CHECK_LAUNCH("copy_diag_inverse");
-  for (int64_t ib = 1; ib < nblk; ++ib) {
-    const int64_t r0 = ib * CB;
-    const int rb = (int)std::min<int64_t>(CB, n - r0);
-    // T (rb x r0) = L[r0:r0+rb, 0:r0] * Linv[0:r0, 0:r0]
-    VecSet a{L + r0, ldl, nullptr};      // M-major: vector k = column k of L, offset r0
-    VecSet b{Linv, ldi, nullptr};        // K-major: vector n = column n of Linv
-    int rc = gemm_run(false, true, rb, r0, r0, a, b, (ldl % 2 == 0) && (ldi % 2 == 0) && (r0 % 2 == 0), 1.0, 0.0, T,
-                      CB, nullptr, nullptr, nullptr, 0, 0, ws, ws_bytes, st);
-    if (rc) return rc;
-    // Linv[r0:r0+rb, 0:r0] = -Linv_ii * T ; A(m,k) = Linv_ii(m,k) = X[m][k] = Dinv[m*CB + k] -> K-major vector m
-    const double* Di = Dinv + ib * CB * CB;
-    VecSet a2{Di, CB, nullptr};
-    VecSet b2{T, CB, nullptr};           // K-major: vector n = column n of T
-    rc = gemm_run(true, true, rb, r0, rb, a2, b2, true, -1.0, 0.0, Linv + r0, ldi, nullptr, nullptr, nullptr, 0, 0,
-                  ws, ws_bytes, st);
-    if (rc) return rc;
-  }
-  return HP_OK;
+  return chol_inv_rec(C, ldc, 0, n, Linv, ldi, T, (n + 1) & ~int64_t(1), info, ws, ws_bytes, st);
 }
 
 // ------------------------------------------------------------------ layout helpers

@@ -53,6 +53,7 @@ struct Params {
   double* red_v;    // per-CTA argmax partials
   int* red_i;
   int* rank;        // device: number of columns factored so far (stops growing at tol)
+  double* Lrm;      // m x PB row-major copy of the current panel of L (pivot-row fetches)
   double tol;
   int k0, k1;       // panel columns [k0, k1)
 };
@@ -100,8 +101,13 @@ __device__ __forceinline__ void local_argmax(const Params& p, int64_t r0, int64_
 }
 
 // One grid-wide barrier per column: the argmax partials for column j+1 are produced in the
-// same pass that computes column j (double-buffered by column parity).
+// same pass that computes column j (double-buffered by column parity).  SROWS: the CTA's rows
+// of the current panel of L live in shared memory (column-major, `per` rows), so the update
+// dot products read shared memory instead of chasing the panel columns through L2; the
+// pivot row comes from the row-major panel copy (one contiguous read).
+template <bool SROWS>
 __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
+  extern __shared__ double s_rows[];
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[PT / 32];
   __shared__ int si[PT / 32];
@@ -149,9 +155,11 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
     // uniform across the grid (every CTA reduced the same partials); rank stays j.
     if (!(dp > p.tol)) return;
     const double ljj = sqrt(dp);
-    for (int t = p.k0 + tid; t < j; t += PT) s_lp[t - p.k0] = __ldcg(p.L + (int64_t)t * p.ldl + pv);
+    for (int t = p.k0 + tid; t < j; t += PT)
+      s_lp[t - p.k0] = SROWS ? __ldcg(p.Lrm + (int64_t)pv * PB + (t - p.k0)) : __ldcg(p.L + (int64_t)t * p.ldl + pv);
     __syncthreads();
     const double* acol = p.A + (int64_t)pv * p.lda;
+    const double rl = 1.0 / ljj;
     for (int64_t i = r0 + tid; i < r1; i += PT) {
       double li;
       if (i == pv) {
@@ -161,11 +169,20 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
         li = 0.0;  // already pivoted: L is lower triangular in pivot order
       } else {
         double s = acol[i];
-        for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
-        li = s / ljj;
+        if (SROWS) {
+          const double* sr = s_rows + (i - r0);
+          for (int t = 0; t < j - p.k0; ++t) s -= sr[(int64_t)t * per] * s_lp[t];
+        } else {
+          for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
+        }
+        li = s * rl;
         p.d[i] -= li * li;
       }
       p.L[(int64_t)j * p.ldl + i] = li;
+      if (SROWS) {
+        s_rows[(int64_t)(j - p.k0) * per + (i - r0)] = li;
+        p.Lrm[i * PB + (j - p.k0)] = li;
+      }
     }
     if (tid == 0 && pv >= r0 && pv < r1) p.piv[j] = pv;
     if (blockIdx.x == 0 && tid == 0) *p.rank = j + 1;
@@ -236,6 +253,7 @@ size_t pstrf_workspace_bytes(int64_t m) {
   o += al((size_t)m * 8);                       // d
   o += al(2048 * 8) + al(2048 * 4) + al(64);    // partials (2 x 1024) + rank + scal
   o += 2 * al((size_t)m * 8);                   // power-iteration vectors
+  o += al((size_t)m * pc::PB * 8);              // row-major panel copy
   o += al(gemm_workspace_bytes(m, m, pc::PB, 1, 0));
   return o;
 }
@@ -268,6 +286,8 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   o += al((size_t)m * 8);
   double* py = reinterpret_cast<double*>(base + o);
   o += al((size_t)m * 8);
+  double* Lrm = reinterpret_cast<double*>(base + o);
+  o += al((size_t)m * PB * 8);
   void* gws = base + o;
   const size_t gwsb = ws_bytes - o;
 
@@ -297,10 +317,21 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   int dev = 0, nsm = 148, per_sm = 1;
   HP_CHECK_CUDA(cudaGetDevice(&dev));
   HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pstrf_panel, PT, 0));
+  // one CTA per SM (at most one per 64 rows); the CTA's panel rows in shared memory when they fit
   const int rows_per_cta = 64;
-  int grid = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), ceil_div(m, rows_per_cta));
+  int grid = (int)std::min<int64_t>((int64_t)nsm, ceil_div(m, rows_per_cta));
   grid = std::max(1, std::min(grid, 1024));
+  const int64_t per = ceil_div(m, grid);
+  const size_t rows_smem = (size_t)per * PB * 8;
+  const bool srows = rows_smem <= 200 * 1024;
+  static bool configured = false;
+  if (!configured) {
+    HP_CHECK_CUDA(cudaFuncSetAttribute(pstrf_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, srows ? (const void*)pstrf_panel<true> : (const void*)pstrf_panel<false>, PT, srows ? rows_smem : 0));
+  HP_REQUIRE(per_sm >= 1, "pstrf: the panel kernel does not fit on an SM");
 
   Params p{};
   p.A = A;
@@ -313,13 +344,17 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   p.red_v = red_v;
   p.red_i = red_i;
   p.rank = rank;
+  p.Lrm = Lrm;
   p.tol = std::max(tol_rel * host_scal, tol_lam * host_lam);
   int host_rank = 0;
   for (int64_t k0 = 0; k0 < m; k0 += PB) {
     p.k0 = (int)k0;
     p.k1 = (int)std::min<int64_t>(m, k0 + PB);
     void* args[] = {&p};
-    HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel, grid, PT, args, 0, st));
+    if (srows)
+      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel<true>, grid, PT, args, rows_smem, st));
+    else
+      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel<false>, grid, PT, args, 0, st));
     count_launches(1);
     HP_CHECK_CUDA(cudaMemcpyAsync(&host_rank, rank, sizeof(int), cudaMemcpyDeviceToHost, st));
     HP_CHECK_CUDA(cudaStreamSynchronize(st));
