@@ -510,7 +510,21 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
                     # any orthonormal basis of span(X) serves Rayleigh-Ritz: Bjorck / Newton-Schulz steps
                     # X <- X (3 I - X^T X) / 2 (two DMMA GEMMs each, no sequential factorisation) while
                     # the drift is small, CholQR otherwise
-                    drift_x = _orthonormalise_basis(X, ws, st, ph)
+                    drift_x = None
+                    # the trailing columns of X (eigenpairs near the polish floor, where Q0 is least
+                    # accurate) can be numerically dependent; CholQR keeps nested spans, so on a
+                    # breakdown the basis is shortened from the tail -- never below the eigenpairs
+                    # above the Gram cutoff plus half the margin -- and orthonormalised again
+                    k_cut = int((lam[:K] >= float(cutoff) * lam_max_h * m).sum().item())
+                    k_min = min(K, k_cut + max(1, (K - k_cut) // 2))
+                    while drift_x is None:
+                        try:
+                            drift_x = _orthonormalise_basis(X, ws, st, ph)
+                        except np.linalg.LinAlgError:
+                            if K <= k_min:
+                                raise
+                            K = max(k_min, K - max(1, (K - k_cut) // 4))
+                            X = X.view_cols(0, K)
                 T = DevMat.empty(m, K)
                 G2 = DevMat.empty(K, K)
                 with _phase("polish_rr", 2.0 * m * m * K + float(m) * K * (K + 1)):

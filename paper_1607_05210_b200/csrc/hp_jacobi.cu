@@ -715,7 +715,11 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   static const bool use_fused = !(getenv("HP_JACOBI_FUSED") && atoi(getenv("HP_JACOBI_FUSED")) == 0);
   HP_CHECK_CUDA(cudaMemsetAsync(p.tile_mark, 0, (size_t)npairs * (npairs + 1) / 2 * 4, st));
   const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, nsm);
-  const unsigned rest_grid = (unsigned)std::min<int64_t>(napply, 2 * (int64_t)nsm);
+  // small problems (leaves, merges) get a grid sized to their work -- about four apply tasks per
+  // CTA, never fewer CTAs than local solves -- so that concurrent node streams do not flood the
+  // SMs with idle apply CTAs; large ones use every SM twice
+  const unsigned rest_grid =
+      (unsigned)std::min<int64_t>(std::max<int64_t>(npairs, ceil_div(napply, 4)), 2 * (int64_t)nsm);
   int stamp = 0;
   for (; sweep < max_sweeps; ++sweep) {
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
