@@ -115,6 +115,15 @@ __device__ __forceinline__ bool needs_rotation(double aij, double aii, double aj
          a > tang * fabs(ajj - aii);
 }
 
+// needs_rotation with the relative test squared (a^2 > tr^2 |a_ii a_jj|): no square root on the
+// rotation's critical path (entries here are far from the under/overflow range of the square)
+__device__ __forceinline__ bool needs_rotation_sq(double aij, double aii, double ajj, double tr, double ta,
+                                                  double floor_ = 0.0, double tang = 0.0) {
+  const double a = fabs(aij);
+  return a > ta && a * a > tr * tr * fabs(aii * ajj) && (floor_ <= 0.0 || fmax(aii, ajj) >= floor_) &&
+         a > tang * fabs(ajj - aii);
+}
+
 // C(64x64) = op(X) * Y with operands in smem, col-major stride TS.
 //  transX = false: X(m,k) at X[k*TS + m];  transX = true: X(m,k) = X[m*TS + k]
 // 8 warps: warp w owns rows (w&3)*16..+16 and cols (w>>2)*32..+32.
@@ -214,73 +223,78 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
   for (int sweep = 0; sweep < p.max_local_sweeps; ++sweep) {
     int rotated = 0;
     for (int step = 0; step < PS - 1; ++step) {
-      // rotation of pair `lane` (computed redundantly by every warp: no broadcast, no barrier)
+      // rotation of pair `lane` (computed redundantly by every warp: no broadcast, no barrier).
+      // Branch-free: non-rotating pairs carry (c, s, t) = (1, 0, 0), which leaves every entry
+      // bit-identical, so all 2x2 updates of a step are independent straight-line code the
+      // compiler can interleave (the former per-pair branches serialised them).
       int a, b;
       circle_pair(PS, step, lane, a, b);
       const double aii = Acur[a * LS + a], ajj = Acur[b * LS + b], aij = Acur[a * LS + b];
-      const int r = needs_rotation(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
-      double c = 1.0, s = 0.0, t = 0.0;
-      if (r) {
+      const int r = needs_rotation_sq(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
+      double c, s, t;
+      {
         // t = sgn(theta) / (|theta| + sqrt(1 + theta^2)), theta = (ajj - aii) / (2 aij), written
         // with one square root and one division: t = 2 aij sgn(d) / (|d| + sqrt(d^2 + 4 aij^2))
         const double dd = ajj - aii, a2 = 2.0 * aij;
-        t = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
-        c = rsqrt(fma(t, t, 1.0));
-        s = t * c;
+        const double tt = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
+        const double cc = rsqrt(fma(tt, tt, 1.0));
+        t = r ? tt : 0.0;
+        c = r ? cc : 1.0;
+        s = r ? tt * cc : 0.0;
       }
       rotated |= r;
-      // A_next = R^T A R : this warp owns row pairs P = warp and warp + 16, column pair Q = lane
+      // A_next = R^T A R : this warp owns row pairs P = warp + NW h, column pair Q = lane; all
+      // operands are loaded before any store
+      {
+        constexpr int NH = 32 / NW;
+        int i1s[NH], j1s[NH];
+        double cps[NH], sps[NH], v[NH][4];
 #pragma unroll
-      for (int h = 0; h < 32 / NW; ++h) {
-        const int P = warp + NW * h;
-        const int rp = __shfl_sync(0xffffffffu, r, P);
-        const double cp = __shfl_sync(0xffffffffu, c, P), sp = __shfl_sync(0xffffffffu, s, P);
-        const int i1 = __shfl_sync(0xffffffffu, a, P), j1 = __shfl_sync(0xffffffffu, b, P);
-        if (P == lane) {
-          const double x00 = Acur[i1 * LS + i1], x11 = Acur[j1 * LS + j1], x01 = Acur[i1 * LS + j1];
-          if (r) {
-            Anx[i1 * LS + i1] = x00 - t * x01;
-            Anx[j1 * LS + j1] = x11 + t * x01;
-            Anx[i1 * LS + j1] = 0.0;
-            Anx[j1 * LS + i1] = 0.0;
-          } else {
-            Anx[i1 * LS + i1] = x00;
-            Anx[j1 * LS + j1] = x11;
-            Anx[i1 * LS + j1] = x01;
-            Anx[j1 * LS + i1] = x01;
-          }
-          continue;
+        for (int h = 0; h < NH; ++h) {
+          const int P = warp + NW * h;
+          cps[h] = __shfl_sync(0xffffffffu, c, P);
+          sps[h] = __shfl_sync(0xffffffffu, s, P);
+          i1s[h] = __shfl_sync(0xffffffffu, a, P);
+          j1s[h] = __shfl_sync(0xffffffffu, b, P);
         }
-        double b00 = Acur[i1 * LS + a], b01 = Acur[i1 * LS + b], b10 = Acur[j1 * LS + a], b11 = Acur[j1 * LS + b];
-        if (rp) {
-          const double n00 = cp * b00 - sp * b10, n01 = cp * b01 - sp * b11;
-          const double n10 = sp * b00 + cp * b10, n11 = sp * b01 + cp * b11;
-          b00 = n00;
-          b01 = n01;
-          b10 = n10;
-          b11 = n11;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          v[h][0] = Acur[i1s[h] * LS + a];
+          v[h][1] = Acur[i1s[h] * LS + b];
+          v[h][2] = Acur[j1s[h] * LS + a];
+          v[h][3] = Acur[j1s[h] * LS + b];
         }
-        if (r) {
-          const double n00 = c * b00 - s * b01, n01 = s * b00 + c * b01;
-          const double n10 = c * b10 - s * b11, n11 = s * b10 + c * b11;
-          b00 = n00;
-          b01 = n01;
-          b10 = n10;
-          b11 = n11;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const bool dg = (warp + NW * h) == lane;
+          const double cp = cps[h], sp = sps[h];
+          const double b00 = v[h][0], b01 = v[h][1], b10 = v[h][2], b11 = v[h][3];
+          const double m00 = cp * b00 - sp * b10, m01 = cp * b01 - sp * b11;
+          const double m10 = sp * b00 + cp * b10, m11 = sp * b01 + cp * b11;
+          const double n00 = c * m00 - s * m01, n01 = s * m00 + c * m01;
+          const double n10 = c * m10 - s * m11, n11 = s * m10 + c * m11;
+          // the pair's own 2x2 block (b00 = a_ii, b01 = b10 = a_ij, b11 = a_jj): exact annihilation
+          const double d00 = b00 - t * b01, d11 = b11 + t * b01, od = r ? 0.0 : b01;
+          const int i1 = i1s[h], j1 = j1s[h];
+          Anx[i1 * LS + a] = dg ? d00 : n00;
+          Anx[i1 * LS + b] = dg ? od : n01;
+          Anx[j1 * LS + a] = dg ? od : n10;
+          Anx[j1 * LS + b] = dg ? d11 : n11;
         }
-        Anx[i1 * LS + a] = b00;
-        Anx[i1 * LS + b] = b01;
-        Anx[j1 * LS + a] = b10;
-        Anx[j1 * LS + b] = b11;
       }
-      // W <- W R on this warp's rows
-      if (r) {
+      // W <- W R on this warp's rows (identity for non-rotating pairs)
+      {
+        constexpr int NR = 64 / NW;
+        double wi[NR], wj[NR];
 #pragma unroll
-        for (int h = 0; h < 64 / NW; ++h) {
-          const int row = warp + NW * h;
-          const double wi = Wl[a * LS + row], wj = Wl[b * LS + row];
-          Wl[a * LS + row] = c * wi - s * wj;
-          Wl[b * LS + row] = s * wi + c * wj;
+        for (int h = 0; h < NR; ++h) {
+          wi[h] = Wl[a * LS + warp + NW * h];
+          wj[h] = Wl[b * LS + warp + NW * h];
+        }
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          Wl[a * LS + warp + NW * h] = c * wi[h] - s * wj[h];
+          Wl[b * LS + warp + NW * h] = s * wi[h] + c * wj[h];
         }
       }
       __syncwarp();
@@ -676,8 +690,12 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   p.tol_abs = tol_abs;
   p.keep_floor = keep_floor;
   p.tol_angle = tol_angle;
-  static const int local_sweeps = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 1;
-  p.max_local_sweeps = local_sweeps;
+  // Local cyclic sweeps per pair: a large matrix in its first (full-apply) phase has its local
+  // solves hidden under the apply of the fused round, so two local sweeps buy fewer outer sweeps
+  // (root H phase 820 -> 778 ms); small problems (leaves, merges) and the nearly diagonal polish
+  // (keep_floor > 0, few active pairs) have the local solve on the critical path: one sweep.
+  static const int local_sweeps_env = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 0;
+  p.max_local_sweeps = local_sweeps_env > 0 ? local_sweeps_env : ((layout(n).nb / 2 >= 32 && keep_floor <= 0.0) ? 2 : 1);
 
   static bool configured = false;
   const int local_smem = 3 * PS * LS * 8;
