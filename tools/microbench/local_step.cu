@@ -221,6 +221,92 @@ __global__ void __launch_bounds__(NT) step_bench(const double* A0, double* out, 
   for (int e = tid; e < PS * PS; e += NT) out[e] = Acur[(e / PS) * LS + e % PS] + Wl[(e / PS) * LS + e % PS];
 }
 
+
+// variant 6: indices computed directly (no shuffles); operands of A and W loaded by every warp
+// while warp 0 computes the 32 rotations into a shared table; barrier; update; barrier
+template <int NT>
+__global__ void __launch_bounds__(NT) step_bench6(const double* A0, double* out, long long* stamps) {
+  constexpr int NW = NT / 32, NH = 32 / NW, NR = 64 / NW;
+  extern __shared__ double dsm[];
+  __shared__ double4 rot[32];   // c, s, t, r
+  double* Acur = dsm;
+  double* Anx = dsm + PS * LS;
+  double* Wl = dsm + 2 * PS * LS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < PS * PS; e += NT) {
+    const int j = e / PS, i = e % PS;
+    Acur[i * LS + j] = A0[j * PS + i];
+    Wl[j * LS + i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  long long acc[5] = {0, 0, 0, 0, 0};
+  for (int step = 0; step < PS - 1; ++step) {
+    long long c0 = clock64();
+    int a, b;
+    circle_pair(PS, step, lane, a, b);
+    int i1s[NH], j1s[NH];
+    double v[NH][4], wi[NR], wj[NR];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) circle_pair(PS, step, warp + NW * h, i1s[h], j1s[h]);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      v[h][0] = Acur[i1s[h] * LS + a];
+      v[h][1] = Acur[i1s[h] * LS + b];
+      v[h][2] = Acur[j1s[h] * LS + a];
+      v[h][3] = Acur[j1s[h] * LS + b];
+    }
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+      wi[h] = Wl[a * LS + warp + NW * h];
+      wj[h] = Wl[b * LS + warp + NW * h];
+    }
+    if (warp == 0) {
+      const double aii = Acur[a * LS + a], ajj = Acur[b * LS + b], aij = Acur[a * LS + b];
+      const int r = fabs(aij) > 1e-300 && aij * aij > 1e-32 * fabs(aii * ajj);
+      const double dd = ajj - aii, a2 = 2.0 * aij;
+      const double tt = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
+      const double cc = rsqrt(fma(tt, tt, 1.0));
+      rot[lane] = make_double4(r ? cc : 1.0, r ? tt * cc : 0.0, r ? tt : 0.0, r ? 1.0 : 0.0);
+    }
+    long long c1 = clock64();
+    __syncthreads();
+    const double4 mine = rot[lane];
+    const double c = mine.x, s = mine.y, t = mine.z;
+    const bool r = mine.w != 0.0;
+    long long c2 = clock64();
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      const bool dg = (warp + NW * h) == lane;
+      const double4 rp = rot[warp + NW * h];
+      const double cp = rp.x, sp = rp.y;
+      const double b00 = v[h][0], b01 = v[h][1], b10 = v[h][2], b11 = v[h][3];
+      const double m00 = cp * b00 - sp * b10, m01 = cp * b01 - sp * b11;
+      const double m10 = sp * b00 + cp * b10, m11 = sp * b01 + cp * b11;
+      const double n00 = c * m00 - s * m01, n01 = s * m00 + c * m01;
+      const double n10 = c * m10 - s * m11, n11 = s * m10 + c * m11;
+      const double d00 = b00 - t * b01, d11 = b11 + t * b01, od = r ? 0.0 : b01;
+      const int i1 = i1s[h], j1 = j1s[h];
+      Anx[i1 * LS + a] = dg ? d00 : n00;
+      Anx[i1 * LS + b] = dg ? od : n01;
+      Anx[j1 * LS + a] = dg ? od : n10;
+      Anx[j1 * LS + b] = dg ? d11 : n11;
+    }
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+      Wl[a * LS + warp + NW * h] = c * wi[h] - s * wj[h];
+      Wl[b * LS + warp + NW * h] = s * wi[h] + c * wj[h];
+    }
+    long long c3 = clock64();
+    double* tmp = Acur; Acur = Anx; Anx = tmp;
+    __syncthreads();
+    long long c4 = clock64();
+    acc[0] += c1 - c0; acc[1] += c2 - c1; acc[2] += c3 - c2; acc[3] += c4 - c3; acc[4] += c4 - c0;
+  }
+  if (lane == 0 && (warp == 0 || warp == NW - 1))
+    for (int k = 0; k < 5; ++k) stamps[(warp == 0 ? 0 : 5) + k] = acc[k];
+  for (int e = tid; e < PS * PS; e += NT) out[e] = Acur[(e / PS) * LS + e % PS] + Wl[(e / PS) * LS + e % PS];
+}
+
 int main() {
   double h[PS * PS];
   srand(1);
@@ -233,7 +319,7 @@ int main() {
   cudaFuncSetAttribute(step_bench<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(step_bench<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* nm[5] = {"rotation", "2x2 blocks", "W update", "barrier", "step total"};
-  for (int variant = 0; variant < 6; ++variant) {
+  for (int variant = 4; variant < 6; ++variant) {
     for (int rep = 0; rep < 2; ++rep) {
       step_bench<256><<<1, 256, smem>>>(dA, dout, st, variant);
       cudaDeviceSynchronize();
@@ -247,6 +333,15 @@ int main() {
     printf("NT=512 variant %d\n", variant);
     for (int k = 0; k < 5; ++k) printf("  %-12s %8.1f | %8.1f\n", nm[k], st[k] / 63.0, st[5 + k] / 63.0);
   }
+  cudaFuncSetAttribute(step_bench6<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(step_bench6<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* nm6[5] = {"loads+rot", "barrier 1", "update", "barrier 2", "step total"};
+  for (int rep = 0; rep < 2; ++rep) { step_bench6<256><<<1, 256, smem>>>(dA, dout, st); cudaDeviceSynchronize(); }
+  printf("NT=256 variant 6\n");
+  for (int k = 0; k < 5; ++k) printf("  %-12s %8.1f | %8.1f\n", nm6[k], st[k] / 63.0, st[5 + k] / 63.0);
+  for (int rep = 0; rep < 2; ++rep) { step_bench6<512><<<1, 512, smem>>>(dA, dout, st); cudaDeviceSynchronize(); }
+  printf("NT=512 variant 6\n");
+  for (int k = 0; k < 5; ++k) printf("  %-12s %8.1f | %8.1f\n", nm6[k], st[k] / 63.0, st[5 + k] / 63.0);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

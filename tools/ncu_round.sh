@@ -9,7 +9,7 @@ set -u
 R=${1:-r1}
 O=gpurun_out
 mkdir -p $O
-HP_PROFILE_RANGE=1 timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+HP_PROFILE_RANGE=1 timeout 1500 ncu --profile-from-start off -c 10000 --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/${R}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > $O/${R}_ncu_bench.log 2>&1
 echo "launch list rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_ --launch-skip 1 -c 1 \
