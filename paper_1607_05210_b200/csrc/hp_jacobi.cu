@@ -136,20 +136,22 @@ __device__ __forceinline__ void mm64(const double* X, const double* Y, double (&
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 4
+  // per-thread fragment base pointers; the fully unrolled k loop then addresses shared memory
+  // with immediate offsets (no per-step index arithmetic between the loads and the DMMAs)
+  const double* xa0 = TRANSX ? X + (r0 + g) * SX + t : X + t * SX + r0 + g;
+  const double* xa1 = TRANSX ? xa0 + 8 * SX : xa0 + 8;
+  const double* yb = Y + (c0 + g) * SY + t;
+  constexpr int XK = TRANSX ? 1 : SX;  // stride of k in X
+#pragma unroll
   for (int k0 = 0; k0 < PS; k0 += 4) {
-    double a[2], b[4];
+    const double a0 = xa0[k0 * XK], a1 = xa1[k0 * XK];
+    double b[4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int m = r0 + i * 8 + g, kk = k0 + t;
-      a[i] = TRANSX ? X[m * SX + kk] : X[kk * SX + m];
-    }
+    for (int j = 0; j < 4; ++j) b[j] = yb[j * 8 * SY + k0];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = Y[(c0 + j * 8 + g) * SY + k0 + t];
+    for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[0][j], a0, b[j]);
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+    for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j], a1, b[j]);
   }
 }
 
@@ -466,6 +468,7 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
 }
 
 __device__ __forceinline__ void rest_tasks(const Params& p, double* X, double* WQ, double* WP);
+
 
 // Persistent apply: a fixed grid (2 CTAs per SM) walks all tasks; tasks of pairs that
 // needed no rotation cost two flag loads instead of a CTA launch.
