@@ -387,6 +387,59 @@ __device__ __forceinline__ void load_slab(double* dst, const double* V, int64_t 
   }
 }
 
+// Result tile (mm64 fragment layout: acc[i][j][e] = C[r0 + 8i + g][c0 + 8j + 2t + e]) straight from
+// the accumulators to global memory.  G tile (rows of pair (rp, rq), columns of pair (cp_, cq)):
+// the tile and its mirror (the mirror as 16-byte stores of two consecutive rows); a diagonal
+// tile writes only its r <= c entries, both ways, so G stays exactly symmetric.
+__device__ __forceinline__ void write_acc_g(const Params& p, const double (&acc)[2][4][2], int rp, int rq, int cp_,
+                                            int cq, bool diag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + i * 8 + g;
+    const int64_t ri = local_index(rp, rq, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + j * 8 + 2 * t;
+      const int64_t ci = local_index(cp_, cq, c);
+      const double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (!diag) {
+        p.G[ci * p.np + ri] = v0;
+        p.G[(ci + 1) * p.np + ri] = v1;
+        *reinterpret_cast<double2*>(p.G + ri * p.np + ci) = make_double2(v0, v1);
+      } else {
+        if (r <= c) {
+          p.G[ci * p.np + ri] = v0;
+          p.G[ri * p.np + ci] = v0;
+        }
+        if (r <= c + 1) {
+          p.G[(ci + 1) * p.np + ri] = v1;
+          p.G[ri * p.np + ci + 1] = v1;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void write_acc_v(const Params& p, const double (&acc)[2][4][2], int cp_, int cq,
+                                            int64_t row0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16, c0 = (warp >> 2) * 32;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + j * 8 + 2 * t;
+    double* v = p.V + local_index(cp_, cq, c) * p.np + row0 + r0 + g;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      v[i * 8] = acc[i][j][0];
+      v[p.np + i * 8] = acc[i][j][1];
+    }
+  }
+}
+
 // One task of the apply step (a G tile or a V slab); returns after its stores.
 __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t ng, int npairs, double* X,
                                            double* WQ, double* WP, int& wq_loaded) {
@@ -413,33 +466,16 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
     __syncthreads();
     if (fQ) {
       mm64<false>(X, WQ, acc);  // X W_Q
-      __syncthreads();
-      store_acc(X, acc);
-      __syncthreads();
-    }
-    if (fP) {
-      mm64<true>(WP, X, acc);   // W_P^T X
-      __syncthreads();
-      store_acc(X, acc);
-      __syncthreads();
-    }
-    if (P == Q) {
-      // diagonal tile: keep G exactly symmetric (upper triangle mirrored)
-      for (int e = threadIdx.x; e < PS * PS; e += AT) {
-        const int j = e / PS, i = e % PS;
-        const double v = i <= j ? X[j * TS + i] : X[i * TS + j];
-        p.G[local_index(pp, pq, j) * p.np + local_index(pp, pq, i)] = v;
+      if (!fP) {
+        write_acc_g(p, acc, pp, pq, qp, qq, P == Q);
+        return;
       }
-      return;
+      __syncthreads();
+      store_acc(X, acc);
+      __syncthreads();
     }
-    for (int e = threadIdx.x; e < PS * PS; e += AT) {
-      const int j = e / PS, i = e % PS;
-      p.G[local_index(qp, qq, j) * p.np + local_index(pp, pq, i)] = X[j * TS + i];
-    }
-    for (int e = threadIdx.x; e < PS * PS; e += AT) {
-      const int i = e / PS, j = e % PS;
-      p.G[local_index(pp, pq, i) * p.np + local_index(qp, qq, j)] = X[j * TS + i];
-    }
+    mm64<true>(WP, X, acc);     // W_P^T X  (fP set here)
+    write_acc_g(p, acc, pp, pq, qp, qq, P == Q);
     return;
   }
   // V slab: rows [rc*64, rc*64+64), columns of pair Q (Q-major, so consecutive tasks share W_Q)
@@ -458,13 +494,7 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
   cp_async_wait<0>();
   __syncthreads();
   mm64<false>(X, WQ, acc);
-  __syncthreads();
-  store_acc(X, acc);
-  __syncthreads();
-  for (int e = threadIdx.x; e < PS * PS; e += AT) {
-    const int j = e / PS, i = e % PS;
-    p.V[local_index(qp, qq, j) * p.np + rc * PS + i] = X[j * TS + i];
-  }
+  write_acc_v(p, acc, qp, qq, rc * PS);
 }
 
 __device__ __forceinline__ void rest_tasks(const Params& p, double* X, double* WQ, double* WP);
