@@ -14,11 +14,11 @@
 // method of snapshots.
 //
 // Kernel structure, per panel of PB columns:
-//   pstrf_panel : cooperative persistent kernel (one CTA per SM).  For each
+//   pstrf_panel_sm : cooperative persistent kernel (one CTA per SM).  For each
 //                 column j: grid-wide argmax of the running diagonal d
 //                 (ties -> smallest index), L[:, j] = (A[:, p] - L_panel L_panel[p]^T)
 //                 / sqrt(d_p) over the CTA's row slice, d -= L[:, j]^2.
-//                 Two grid.sync() per column.
+//                 One grid.sync() per column.
 //   trailing    : A -= L_panel L_panel^T (full m x m, symmetric) on the DMMA
 //                 GEMM engine.
 #include <cooperative_groups.h>
@@ -101,13 +101,9 @@ __device__ __forceinline__ void local_argmax(const Params& p, int64_t r0, int64_
 }
 
 // One grid-wide barrier per column: the argmax partials for column j+1 are produced in the
-// same pass that computes column j (double-buffered by column parity).  SROWS: the CTA's rows
-// of the current panel of L live in shared memory (column-major, `per` rows), so the update
-// dot products read shared memory instead of chasing the panel columns through L2; the
-// pivot row comes from the row-major panel copy (one contiguous read).
-template <bool SROWS>
+// same pass that computes column j (double-buffered by column parity).  Global-memory form,
+// used only when a CTA's rows of the panel do not fit in shared memory (pstrf_panel_sm).
 __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
-  extern __shared__ double s_rows[];
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[PT / 32];
   __shared__ int si[PT / 32];
@@ -156,7 +152,7 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
     if (!(dp > p.tol)) return;
     const double ljj = sqrt(dp);
     for (int t = p.k0 + tid; t < j; t += PT)
-      s_lp[t - p.k0] = SROWS ? __ldcg(p.Lrm + (int64_t)pv * PB + (t - p.k0)) : __ldcg(p.L + (int64_t)t * p.ldl + pv);
+      s_lp[t - p.k0] = __ldcg(p.L + (int64_t)t * p.ldl + pv);
     __syncthreads();
     const double* acol = p.A + (int64_t)pv * p.lda;
     const double rl = 1.0 / ljj;
@@ -169,20 +165,11 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
         li = 0.0;  // already pivoted: L is lower triangular in pivot order
       } else {
         double s = acol[i];
-        if (SROWS) {
-          const double* sr = s_rows + (i - r0);
-          for (int t = 0; t < j - p.k0; ++t) s -= sr[(int64_t)t * per] * s_lp[t];
-        } else {
-          for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
-        }
+        for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
         li = s * rl;
         p.d[i] -= li * li;
       }
       p.L[(int64_t)j * p.ldl + i] = li;
-      if (SROWS) {
-        s_rows[(int64_t)(j - p.k0) * per + (i - r0)] = li;
-        p.Lrm[i * PB + (j - p.k0)] = li;
-      }
     }
     if (tid == 0 && pv >= r0 && pv < r1) p.piv[j] = pv;
     if (blockIdx.x == 0 && tid == 0) *p.rank = j + 1;
@@ -190,6 +177,144 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
     local_argmax(p, r0, r1, slot ^ 1, sv, si);  // partials for column j+1
     grid.sync();
   }
+}
+
+// The shared-memory form of pstrf_panel (the CTA's rows of the panel fit in shared memory):
+// per column, the critical path between two grid barriers is
+//   reduce the argmax partials -> fetch the pivot row of the panel (and, overlapped with it,
+//   this thread's entry of the pivot column of A) -> the update dot products -> the CTA's
+//   argmax partial for the next column.
+// The running diagonal of the CTA's rows lives in shared memory for the whole panel (written
+// back on exit), the dot products are split over RT threads per row (RT independent partial
+// sums, combined by shuffles in a fixed order) and the argmax partial is one warp's reduction
+// of shared memory.  Same pivots and the same factor up to the summation order of the dots.
+constexpr int RT = 4;  // threads per row in the update dot products
+__global__ void __launch_bounds__(PT) pstrf_panel_sm(Params p) {
+  extern __shared__ double s_rows[];
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_dp;
+  __shared__ int s_p;
+  __shared__ double s_lp[PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nblk = gridDim.x;
+  const int64_t per = (p.m + nblk - 1) / nblk;
+  const int64_t r0 = blockIdx.x * per, r1 = min(p.m, r0 + per);
+  const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
+  double* s_d = s_rows + (int64_t)per * PB;  // running diagonal of rows [r0, r1)
+  for (int i = tid; i < nr; i += PT) s_d[i] = p.d[r0 + i];
+  __syncthreads();
+  // warp 0: argmax of s_d (ties -> smallest index) -> partials[slot][blockIdx.x]
+  auto cta_argmax = [&](int slot) {
+    if (warp != 0) return;
+    double bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = lane; i < nr; i += 32) {
+      const double v = s_d[i];
+      if (better(v, (int)(r0 + i), bv, bi)) {
+        bv = v;
+        bi = (int)(r0 + i);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      p.red_v[slot * 1024 + blockIdx.x] = bv;
+      p.red_i[slot * 1024 + blockIdx.x] = bi;
+    }
+  };
+  auto write_back = [&]() {
+    for (int i = tid; i < nr; i += PT) p.d[r0 + i] = s_d[i];
+  };
+  cta_argmax(p.k0 & 1);
+  grid.sync();
+  const int sub = tid % RT;
+  for (int j = p.k0; j < p.k1; ++j) {
+    const int slot = j & 1;
+    if (warp == 0) {
+      double gv = -INFINITY;
+      int gi = 0x7fffffff;
+      for (int b = lane; b < (int)nblk; b += 32) {
+        const double v = __ldcg(p.red_v + slot * 1024 + b);
+        const int ii = __ldcg(p.red_i + slot * 1024 + b);
+        if (better(v, ii, gv, gi)) {
+          gv = v;
+          gi = ii;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        if (better(ov, oi, gv, gi)) {
+          gv = ov;
+          gi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_dp = gv;
+        s_p = gi;
+      }
+    }
+    __syncthreads();
+    const double dp = s_dp;
+    const int pv = s_p;
+    if (!(dp > p.tol)) {  // uniform across the grid: the remaining pivots are rounding noise
+      write_back();
+      return;
+    }
+    const double ljj = sqrt(dp);
+    const int nj = j - p.k0;
+    for (int t = tid; t < nj; t += PT) s_lp[t] = __ldcg(p.Lrm + (int64_t)pv * PB + t);
+    // this thread's first row's entry of the pivot column, in flight with the pivot-row fetch
+    const double* acol = p.A + (int64_t)pv * p.lda;
+    const int row_first = tid / RT;
+    double a_first = 0.0;
+    if (sub == 0 && row_first < nr) a_first = acol[r0 + row_first];
+    __syncthreads();
+    const double rl = 1.0 / ljj;
+    for (int rb = 0; rb < nr; rb += PT / RT) {
+      const int il = rb + tid / RT;  // local row (uniform within a group of RT lanes)
+      const bool live = il < nr;
+      const int64_t i = r0 + il;
+      const double di = live ? s_d[il] : -INFINITY;
+      const bool upd = live && i != pv && di != -INFINITY;
+      double part = 0.0;
+      if (upd) {
+        const double* sr = s_rows + il;
+        for (int t = sub; t < nj; t += RT) part = fma(-sr[(int64_t)t * per], s_lp[t], part);
+      }
+      // fixed-order combination of the RT partial sums (lanes of a group are consecutive)
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (live && sub == 0) {
+        double li;
+        if (i == pv) {
+          li = ljj;
+          s_d[il] = -INFINITY;
+        } else if (di == -INFINITY) {
+          li = 0.0;  // already pivoted: L is lower triangular in pivot order
+        } else {
+          const double a = rb == 0 ? a_first : acol[i];
+          li = (a + part) * rl;
+          s_d[il] = di - li * li;
+        }
+        p.L[(int64_t)j * p.ldl + i] = li;
+        s_rows[(int64_t)nj * per + il] = li;
+        p.Lrm[i * PB + nj] = li;
+      }
+    }
+    if (tid == 0 && pv >= r0 && pv < r1) p.piv[j] = pv;
+    if (blockIdx.x == 0 && tid == 0) *p.rank = j + 1;
+    __syncthreads();
+    cta_argmax(slot ^ 1);  // partials for column j+1
+    grid.sync();
+  }
+  write_back();
 }
 
 __global__ void diag_init(const double* G, int64_t ldg, int64_t m, double* A, int64_t lda, double* d) {
@@ -322,15 +447,15 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   int grid = (int)std::min<int64_t>((int64_t)nsm, ceil_div(m, rows_per_cta));
   grid = std::max(1, std::min(grid, 1024));
   const int64_t per = ceil_div(m, grid);
-  const size_t rows_smem = (size_t)per * PB * 8;
+  const size_t rows_smem = (size_t)per * (PB + 1) * 8;  // panel rows + running diagonal
   const bool srows = rows_smem <= 200 * 1024;
   static bool configured = false;
   if (!configured) {
-    HP_CHECK_CUDA(cudaFuncSetAttribute(pstrf_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HP_CHECK_CUDA(cudaFuncSetAttribute(pstrf_panel_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
   HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, srows ? (const void*)pstrf_panel<true> : (const void*)pstrf_panel<false>, PT, srows ? rows_smem : 0));
+      &per_sm, srows ? (const void*)pstrf_panel_sm : (const void*)pstrf_panel, PT, srows ? rows_smem : 0));
   HP_REQUIRE(per_sm >= 1, "pstrf: the panel kernel does not fit on an SM");
 
   Params p{};
@@ -352,9 +477,9 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
     p.k1 = (int)std::min<int64_t>(m, k0 + PB);
     void* args[] = {&p};
     if (srows)
-      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel<true>, grid, PT, args, rows_smem, st));
+      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel_sm, grid, PT, args, rows_smem, st));
     else
-      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel<false>, grid, PT, args, 0, st));
+      HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel, grid, PT, args, 0, st));
     count_launches(1);
     HP_CHECK_CUDA(cudaMemcpyAsync(&host_rank, rank, sizeof(int), cudaMemcpyDeviceToHost, st));
     HP_CHECK_CUDA(cudaStreamSynchronize(st));
