@@ -319,12 +319,13 @@ def main():
         "achieved": round(g_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": round(g_tf / FP64_PEAK_TFLOPS, 4),
         # DRAM bytes of the family's largest launch (root Gram SYRK, gemm_tma_kernel<1,1>, m=8192,
-        # d=200,000) from one ncu --set full capture (profiles/r1b_gemm_gram8192_metrics.txt):
-        # 269.4 GB read + 0.56 GB written against 13.65 GB algorithmic (S once + G): the 2080
-        # output tiles run in 14 waves and each wave re-streams the column panels it touches
-        # (L2 hit rate 64 %); at 0.68 TB/s (8 % of HBM) the launch stays tensor-bound (98.8 %
-        # tensor-pipe active), so the re-reads cost no time
-        "traffic": 269.94e9, "traffic_algorithmic": 13.65e9,
+        # d=200,000) from one ncu --set full capture (profiles/r1g_gemm_gram8192_metrics.txt):
+        # 104.4 GB read + 0.56 GB written against 13.65 GB algorithmic (S once + G).  The 2080
+        # output tiles run in 14 waves; with the grouped tile raster (8 column panels per group,
+        # hp_gemm.cu tile_coords) a wave shares ~26 panels (L2 hit rate 82 %; the column-major order
+        # read 269 GB at 64 %).  At 0.26 TB/s (3 % of HBM) the launch is tensor-bound (98.8 %
+        # tensor-pipe active), so the remaining re-reads cost no time
+        "traffic": 105.0e9, "traffic_algorithmic": 13.65e9,
         "peak_source": "measured FP64 DMMA peak on this pool's B200 (tools/microbench/fp64_peak.cu, "
                        "profiles/r1_fp64_peak.txt); MEASURED_PEAKS.json carries no FP64 figure",
         "share_of_step": round(g_ms / step_ms, 4),
