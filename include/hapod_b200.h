@@ -165,6 +165,12 @@ int hp_transpose_rm_to_cm(const double* src, int64_t rows, int64_t cols, double*
 int hp_scale(const double* src, int64_t lds, int64_t rows, int64_t cols, const double* row_mul, const double* row_div,
              const double* col_mul, double* dst, int64_t ldd, void* stream);
 int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, void* stream);
+/* Stream-ordered read of `bytes` (multiple of 4) device bytes into PINNED host memory by a kernel
+   (no copy engine: a D2H memcpy queues behind pending host-to-device uploads).  The host side of
+   every small read-back on the node path -- the finiteness flag of SnapshotBlock (pod.py:115-116),
+   the truncation counts of _from_spectrum (pod.py:284-289), the drift of _finish_modes
+   (pod.py:245-247) and the singular values of the ModeSet (pod.py:142-154). */
+int hp_read_small(const void* src, void* pinned_dst, int64_t bytes, void* stream);
 /* C(i,i) += s for i < n (Bjorck / Newton-Schulz orthonormalisation of the Ritz basis). */
 int hp_add_diag(double* C, int64_t ldc, int64_t n, double s, void* stream);
 

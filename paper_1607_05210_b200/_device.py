@@ -188,6 +188,13 @@ class DevMat:
 
 
 _COPY_STREAM = None
+_COPY_LOCK = threading.Lock()
+_COPY_INFLIGHT: list = []   # completion events of the uploads queued on the copy stream
+# at most this many uploads queued at once: any device-to-host read (a memcpy, or a kernel writing
+# pinned memory) waits behind the copy engine's pending host-to-device work, so an unbounded queue
+# (all 16 leaves of config 1 request their 0.8 GB upload at once) stalls every leaf's first host
+# read-back for most of the 13 GB transfer; two in flight keep the DMA engine busy
+COPY_MAX_INFLIGHT = int(_os.environ.get("HP_COPY_MAX_INFLIGHT", "2"))
 
 
 def copy_stream():
@@ -226,10 +233,20 @@ def upload(values, check_finite: bool = True, via=None) -> DevMat:
             dst = out.storage[: out.ld * m].view(m, out.ld)[:, :d]
             if via is not None and not t.is_cuda:
                 cur = torch.cuda.current_stream()
-                via.wait_stream(cur)  # the destination was allocated on the current stream
-                with torch.cuda.stream(via):
-                    dst.copy_(src, non_blocking=True)
-                cur.wait_stream(via)
+                # the copy and the event that marks ITS completion are enqueued atomically: with
+                # `cur.wait_stream(via)` a worker could also wait for copies other workers enqueued
+                # in between (all 16 leaves of config 1 request their upload at once), i.e. for
+                # the whole 13 GB transfer before its first kernel
+                with _COPY_LOCK:
+                    while len(_COPY_INFLIGHT) >= max(1, COPY_MAX_INFLIGHT):
+                        _COPY_INFLIGHT.pop(0).synchronize()
+                    via.wait_stream(cur)  # the destination was allocated on the current stream
+                    with torch.cuda.stream(via):
+                        dst.copy_(src, non_blocking=True)
+                    done = torch.cuda.Event()
+                    done.record(via)
+                    _COPY_INFLIGHT.append(done)
+                cur.wait_event(done)
             else:
                 dst.copy_(src, non_blocking=True)
         else:                                                  # row-major (or strided) source
@@ -242,9 +259,35 @@ def upload(values, check_finite: bool = True, via=None) -> DevMat:
         if check_finite:
             bad = torch.zeros(1, dtype=torch.int32, device="cuda")
             N.check(lib.hp_finite_check(out.ptr, out.ld, d, m, bad.data_ptr(), _stream()), "finite")
-            if int(bad.item()):
+            if int(host_read(bad)[0]):
                 raise ValueError("snapshot block contains non-finite entries")
     return out
+
+
+_PINNED = threading.local()
+
+
+def host_read(t) -> np.ndarray:
+    """Read a small device tensor on the host: a kernel (hp_read_small) writes it into a
+    per-thread PINNED buffer, then an event of the current stream is awaited.  `.item()` /
+    `.cpu()` -- any device-to-host memcpy, pinned or not -- was measured to queue behind the copy
+    engine's pending host-to-device transfers: under the e2e leg every leaf's finiteness check
+    and truncation read-back waited for most of the 13 GB upload queue."""
+    flat = t.reshape(-1).contiguous()
+    n = flat.numel()
+    bufs = getattr(_PINNED, "bufs", None)
+    if bufs is None:
+        bufs = _PINNED.bufs = {}
+    buf = bufs.get(flat.dtype)
+    if buf is None or buf.numel() < n:
+        buf = bufs[flat.dtype] = torch.empty(max(n, 64), dtype=flat.dtype, pin_memory=True)
+    b = buf[:n]
+    N.check(N.load().hp_read_small(flat.data_ptr(), b.data_ptr(), n * flat.element_size(), _stream()),
+            "read back")
+    ev = torch.cuda.Event()
+    ev.record()
+    ev.synchronize()
+    return b.numpy().copy()
 
 
 def ones(n: int):
@@ -383,7 +426,7 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
     drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
     N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
             "X^T X")
-    drift0 = drift = float(drift_dev.item())
+    drift0 = drift = float(host_read(drift_dev)[0])
     ph.flops += float(m) * K * (K + 1)
     if drift > BJORCK_MAX_DRIFT:
         rws = _ws(lib.hp_reortho_workspace_bytes(m, K))
@@ -405,7 +448,7 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
         X, Y = Y, X
         N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
                 "X^T X")
-        drift = float(drift_dev.item())
+        drift = float(host_read(drift_dev)[0])
         ph.flops += 2.0 * m * K * K + float(m) * K * (K + 1)
     if X is not orig:
         N.check(lib.hp_scale(X.ptr, X.ld, m, K, None, None, None, orig.ptr, orig.ld, st), "copy back")
@@ -487,7 +530,8 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
             info_h = torch.empty(4, dtype=torch.float64, device="cuda")
             N.check(lib.hp_truncate(lam.data_ptr(), r, 0.0, float(cutoff) * POLISH_FACTOR, m, sig_h.data_ptr(),
                                     info_h.data_ptr(), st), "polish count")
-            lam_max_h, K = float(info_h[0].item()), int(info_h[1].item())
+            info_hh = host_read(info_h[:2])
+            lam_max_h, K = float(info_hh[0]), int(info_hh[1])
             if K:
                 # Q0 = L W_K Lambda_K^{-1/2}: approximate eigenvectors of G from the preconditioned solve.
                 # One subspace-iteration step X = G Q0 Lambda_K^{-1} damps the components along
@@ -515,7 +559,7 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
                     # accurate) can be numerically dependent; CholQR keeps nested spans, so on a
                     # breakdown the basis is shortened from the tail -- never below the eigenpairs
                     # above the Gram cutoff plus half the margin -- and orthonormalised again
-                    k_cut = int((lam[:K] >= float(cutoff) * lam_max_h * m).sum().item())
+                    k_cut = int(host_read((lam[:K] >= float(cutoff) * lam_max_h * m).sum())[0])
                     k_min = min(K, k_cut + max(1, (K - k_cut) // 2))
                     while drift_x is None:
                         try:
@@ -554,7 +598,7 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
                                 info.data_ptr(), st), "truncate")
     if KEEP_SPECTRUM:
         LAST_SPECTRUM[:] = [lam[:nev].cpu().numpy()]
-    lam_max, nkeep, n_modes, tail = info.cpu().tolist()
+    lam_max, nkeep, n_modes, tail = host_read(info).tolist()
     nkeep, n_modes = int(nkeep), int(n_modes)
     if not (lam_max > 0.0):
         return EigVectors(lam_max, 0, 0, 0.0, ones(0), None, sweeps)
@@ -634,7 +678,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         N.check(lib.hp_drift(U.ptr, U.ld, d, n_modes, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(),
                              st), "drift")
     del ws
-    drift = float(drift_dev.item())
+    drift = float(host_read(drift_dev)[0])
     reorthed = False
     if drift > DRIFT_TOL:
         ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
@@ -658,7 +702,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     with _phase("signs"):
         N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None,
                              R.ld if R is not None else 0, m if R is not None else 0, None, st), "signs")
-    sig_host = sig_dev.cpu().numpy()
+    sig_host = host_read(sig_dev)
     return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps, m)
 
 
@@ -714,7 +758,7 @@ def residual_energy(S: DevMat, Phi: DevMat | None, sqrt_w=None) -> float:
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
     ws = _ws(lib.hp_sumsq_workspace_bytes())
     N.check(lib.hp_sumsq(X.ptr, X.ld, X.rows, X.cols, out.data_ptr(), ws.data_ptr(), ws.numel(), st), "sumsq")
-    return float(out.item())
+    return float(host_read(out)[0])
 
 
 def block_diag_times(blocks: list, right: DevMat) -> DevMat:

@@ -59,6 +59,7 @@ _SIGNATURES = {
     "hp_transpose_rm_to_cm": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "hp_scale": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "hp_finite_check": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "hp_read_small": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "hp_add_diag": (c_int, [c_vp, c_i64, c_i64, c_dbl, c_vp]),
     "hp_gram_drift": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "hp_col_absmax": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),

@@ -104,7 +104,7 @@ static int cholqr_pass(const double* X, int64_t ldx, int64_t d, int64_t N, doubl
   const int64_t ldn = (N + 1) & ~int64_t(1);
   int rc = chol_inv_run(C, ldc, N, Linv, ldn, T, info, gws, gwsb, st);
   if (rc) return rc;
-  HP_CHECK_CUDA(cudaMemcpyAsync(host_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HP_CHECK_CUDA(d2h_small(host_info, info, sizeof(int), st));
   // Y = X * Linv^T : B(k, n) = Linv(n, k) -> N-major operand (vector k = column k of Linv), upper triangular
   VecSet a{X, ldx, nullptr};
   VecSet b{Linv, ldn, nullptr};
@@ -297,7 +297,7 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
   if (!rc && hinfo[0] != 0) {
     // shifted CholQR (Fukaya et al.): s = 11 (d N + N (N+1)) u ||U||_2^2, ||U||_2^2 <= trace(U^T U)
     trace_kernel<<<1, 256, 0, st>>>(A, ldn, N, C);
-    cudaMemcpyAsync(htrace, C, sizeof(double), cudaMemcpyDeviceToHost, st);
+    d2h_small(htrace, C, sizeof(double), st);
     cudaStreamSynchronize(st);
     const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * 1.1102230246251565e-16 * htrace[0];
     add_diag<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(A, ldn, N, shift);
@@ -365,6 +365,13 @@ int hp_finite_check(const double* src, int64_t lds, int64_t rows, int64_t cols, 
   return finite_check_run(src, lds, rows, cols, bad, (cudaStream_t)stream);
 }
 
+int hp_read_small(const void* src, void* pinned_dst, int64_t bytes, void* stream) {
+  HP_REQUIRE(bytes >= 0 && bytes % 4 == 0, "hp_read_small: size must be a multiple of 4 bytes");
+  HP_CHECK_CUDA(d2h_small(pinned_dst, src, (size_t)bytes, (cudaStream_t)stream));
+  count_launches(1);
+  return HP_OK;
+}
+
 size_t hp_pstrf_workspace_bytes(int64_t m) { return pstrf_workspace_bytes(m); }
 
 int hp_pstrf(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, int* piv, double tol_rel,
@@ -430,10 +437,10 @@ int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl
     for (auto& e : ev) cudaEventDestroy(e);
   }
   if (rc) return rc;
-  int h = 0;
-  HP_CHECK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int* h = reinterpret_cast<int*>(pinned_scratch() + 160);  // pinned: see pstrf_run
+  HP_CHECK_CUDA(d2h_small(h, info, sizeof(int), st));
   HP_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (info_out) *info_out = h;
+  if (info_out) *info_out = *h;
   return HP_OK;
 }
 

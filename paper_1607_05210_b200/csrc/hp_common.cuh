@@ -134,4 +134,45 @@ int num_sms();
 // streams).  Slots: [0, 64) Jacobi sweep counters, [64, 128) re-orthonormalisation flags.
 char* pinned_scratch();
 
+
+// Stream-ordered zero fill as a KERNEL.  cudaMemset*Async can be serviced by a copy engine, where it
+// queues behind unrelated host-to-device transfers (measured: under the e2e leg every leaf's
+// 4-byte flag memset waited for most of the 13 GB upload queue); a kernel only waits for its stream.
+namespace {
+__global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < rows * cols) p[(e / rows) * ld + e % rows] = 0.0;
+}
+__global__ void zero_words_kernel(unsigned* p, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) p[e] = 0u;
+}
+__global__ void copy_words_kernel(unsigned* dst, const unsigned* src, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) dst[e] = src[e];
+}
+}  // namespace
+// bytes must be a multiple of 4 (flags, counters, doubles)
+inline cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
+  const int64_t n = (int64_t)(bytes / 4);
+  if (n == 0) return cudaSuccess;
+  zero_words_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(static_cast<unsigned*>(p), n);
+  return cudaGetLastError();
+}
+// Small device-to-host read into PINNED host memory (device-accessible under UVA) by a kernel:
+// cudaMemcpyAsync D2H -- pinned or pageable -- was measured to queue behind the copy engine's
+// pending host-to-device transfers (the e2e leaf uploads), stalling every leaf's host sync.
+inline cudaError_t d2h_small(void* pinned_dst, const void* src, size_t bytes, cudaStream_t st) {
+  const int64_t n = (int64_t)(bytes / 4);
+  if (n == 0) return cudaSuccess;
+  copy_words_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(static_cast<unsigned*>(pinned_dst),
+                                                                 static_cast<const unsigned*>(src), n);
+  return cudaGetLastError();
+}
+inline cudaError_t zero_2d_async(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  zero_2d_kernel<<<(unsigned)ceil_div(rows * cols, 256), 256, 0, st>>>(p, ld, rows, cols);
+  return cudaGetLastError();
+}
+
 }  // namespace hp

@@ -753,7 +753,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
 
   char* host_buf = pinned_scratch();
   HP_REQUIRE(host_buf != nullptr, "syev: pinned host scratch unavailable");
-  HP_CHECK_CUDA(cudaMemsetAsync(p.mm_count, 0, 8, st));
+  HP_CHECK_CUDA(zero_async(p.mm_count, 8, st));
   int status = HP_ELINALG;
   int sweep = 0;
   double prev_off = INFINITY;
@@ -764,7 +764,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   if (trace > 1)
     for (auto& e : ev) cudaEventCreate(&e);
   static const bool use_fused = !(getenv("HP_JACOBI_FUSED") && atoi(getenv("HP_JACOBI_FUSED")) == 0);
-  HP_CHECK_CUDA(cudaMemsetAsync(p.tile_mark, 0, (size_t)npairs * (npairs + 1) / 2 * 4, st));
+  HP_CHECK_CUDA(zero_async(p.tile_mark, (size_t)npairs * (npairs + 1) / 2 * 4, st));
   const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, nsm);
   // small problems (leaves, merges) get a grid sized to their work -- about four apply tasks per
   // CTA, never fewer CTAs than local solves -- so that concurrent node streams do not flood the
@@ -773,7 +773,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
       (unsigned)std::min<int64_t>(std::max<int64_t>(npairs, ceil_div(napply, 4)), 2 * (int64_t)nsm);
   int stamp = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    cudaError_t e = cudaMemsetAsync(p.counter, 0, 24, st);
+    cudaError_t e = zero_async(p.counter, 24, st);
     if (e != cudaSuccess) break;
     // Per round r: needed(r), then ONE fused launch in which CTAs 0..npairs-1 solve the local
     // problems of round r+1 before joining the dynamically scheduled rest of round r's apply.
@@ -812,7 +812,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
       }
     }
     stamp += R;
-    e = cudaMemcpyAsync(host_buf, p.counter, 32, cudaMemcpyDeviceToHost, st);  // counter, maxoff, mm_count
+    e = d2h_small(host_buf, p.counter, 32, st);  // counter, maxoff, mm_count
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       set_error(std::string("syev sweep: ") + cudaGetErrorString(e));

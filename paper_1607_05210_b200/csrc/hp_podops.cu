@@ -135,7 +135,7 @@ __global__ void drift_kernel(const double* C, int64_t ldc, int64_t n, double* ou
 }
 
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st) {
-  HP_CHECK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  HP_CHECK_CUDA(zero_async(out, sizeof(double), st));
   if (n == 0) return HP_OK;
   const int64_t blocks = std::min<int64_t>(ceil_div(n * n, 256), 4 * 148);
   drift_kernel<<<(unsigned)blocks, 256, 0, st>>>(C, ldc, n, out);
@@ -360,9 +360,9 @@ int64_t chol_t_cols(int64_t n) { return std::max<int64_t>(ceil_div(std::max<int6
 
 int chol_inv_run(double* C, int64_t ldc, int64_t n, double* Linv, int64_t ldi, double* T, int* info, void* ws,
                  size_t ws_bytes, cudaStream_t st) {
-  HP_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  HP_CHECK_CUDA(zero_async(info, sizeof(int), st));
   if (n == 0) return HP_OK;
-  HP_CHECK_CUDA(cudaMemset2DAsync(Linv, ldi * 8, 0, n * 8, n, st));
+  HP_CHECK_CUDA(zero_2d_async(Linv, ldi, n, n, st));
   return chol_inv_rec(C, ldc, 0, n, Linv, ldi, T, (n + 1) & ~int64_t(1), info, ws, ws_bytes, st);
 }
 
@@ -420,7 +420,7 @@ __global__ void finite_kernel(const double* src, int64_t lds, int64_t rows, int6
 }
 
 int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st) {
-  HP_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  HP_CHECK_CUDA(zero_async(bad, sizeof(int), st));
   if (rows == 0 || cols == 0) return HP_OK;
   finite_kernel<<<(unsigned)ceil_div(rows * cols, 256), 256, 0, st>>>(src, lds, rows, cols, bad);
   HP_CHECK_LAUNCH("finite_kernel");

@@ -420,8 +420,15 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   HP_CHECK_LAUNCH("diag_init");
   max_diag_kernel<<<1, 256, 0, st>>>(d, m, scal);
   HP_CHECK_LAUNCH("max_diag");
-  HP_CHECK_CUDA(cudaMemsetAsync(rank, 0, sizeof(int), st));
+  HP_CHECK_CUDA(zero_async(rank, sizeof(int), st));
   // lower bound of lambda_max by power iteration: ||G x|| <= lambda_max for ||x|| = 1
+  // host read-backs through this thread's PINNED scratch: a pageable device-to-host copy can
+  // queue behind unrelated host-to-device transfers (the e2e leaf uploads on the copy stream)
+  char* pin = pinned_scratch();
+  HP_REQUIRE(pin != nullptr, "pstrf: pinned host scratch unavailable");
+  double* pin_lam = reinterpret_cast<double*>(pin + 128);
+  double* pin_scal = reinterpret_cast<double*>(pin + 136);
+  int* pin_rank = reinterpret_cast<int*>(pin + 144);
   double host_lam = 0.0;
   if (tol_lam > 0.0) {
     fill_value<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(px, m, 1.0 / sqrt((double)m));
@@ -432,11 +439,13 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
       normalise<<<1, 256, 0, st>>>(py, m, px, lam_est);
       HP_CHECK_LAUNCH("normalise");
     }
-    HP_CHECK_CUDA(cudaMemcpyAsync(&host_lam, lam_est, sizeof(double), cudaMemcpyDeviceToHost, st));
+    HP_CHECK_CUDA(d2h_small(pin_lam, lam_est, sizeof(double), st));
   }
   double host_scal = 0.0;
-  HP_CHECK_CUDA(cudaMemcpyAsync(&host_scal, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+  HP_CHECK_CUDA(d2h_small(pin_scal, scal, sizeof(double), st));
   HP_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (tol_lam > 0.0) host_lam = *pin_lam;
+  host_scal = *pin_scal;
   if (!(host_scal > 0.0)) return HP_OK;  // all-zero Gramian: rank 0
 
   int dev = 0, nsm = 148, per_sm = 1;
@@ -481,8 +490,9 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
     else
       HP_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)pstrf_panel, grid, PT, args, 0, st));
     count_launches(1);
-    HP_CHECK_CUDA(cudaMemcpyAsync(&host_rank, rank, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HP_CHECK_CUDA(d2h_small(pin_rank, rank, sizeof(int), st));
     HP_CHECK_CUDA(cudaStreamSynchronize(st));
+    host_rank = *pin_rank;
     const int64_t done = host_rank;
     if (done < p.k1 || done >= m) break;
     // trailing update of the whole working matrix: A -= L_panel L_panel^T

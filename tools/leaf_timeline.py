@@ -2,7 +2,10 @@
 start/end of each phase relative to the step start (CUDA events), to see how the leaf wave
 overlaps.
 
-    python tools/leaf_timeline.py [d] [workers]
+    python tools/leaf_timeline.py [d] [workers] [e2e]
+
+e2e: the leaves are column views of a pinned HOST buffer uploaded on demand through the shared
+copy stream (bench.py's e2e leg), so the timeline shows how the 13 GB transfer overlaps the wave.
 """
 import os
 import sys
@@ -19,9 +22,24 @@ workers = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 wl = W.make(1, d=d)
 sp = H.InnerProductSpace(d)
 tree = H.build_star(16)
-leaves = H.distribute_columns(tree, H.SnapshotBlock(sp, wl.values), block_size=512)
+e2e = len(sys.argv) > 3 and sys.argv[3] == "e2e"
+if e2e:
+    host = torch.empty((wl.m, d), dtype=torch.float64, pin_memory=True)
+    host.copy_(wl.values.t())
+    src = host.t()
+else:
+    src = wl.values
+
+
+def make_leaves():
+    return H.distribute_columns(tree, H.SnapshotBlock(sp, src, defer_upload=e2e), block_size=512)
+
+
+leaves = make_leaves()
 tol = H.assign_tolerances(tree, leaves, H.eps_star_to_target(wl.eps_star, wl.m), omega=0.75)
 for rep in range(2):
+    if e2e:
+        leaves = make_leaves()
     D.Profiler.reset(True)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
