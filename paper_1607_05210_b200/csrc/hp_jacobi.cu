@@ -765,7 +765,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     for (auto& e : ev) cudaEventCreate(&e);
   static const bool use_fused = !(getenv("HP_JACOBI_FUSED") && atoi(getenv("HP_JACOBI_FUSED")) == 0);
   HP_CHECK_CUDA(zero_async(p.tile_mark, (size_t)npairs * (npairs + 1) / 2 * 4, st));
-  const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, nsm);
+  const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, 2 * (int64_t)nsm);  // one task per CTA (2 per SM)
   // small problems (leaves, merges) get a grid sized to their work -- about four apply tasks per
   // CTA, never fewer CTAs than local solves -- so that concurrent node streams do not flood the
   // SMs with idle apply CTAs; large ones use every SM twice
