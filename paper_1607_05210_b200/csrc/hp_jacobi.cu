@@ -168,6 +168,30 @@ __device__ __forceinline__ void store_acc(double* C, const double (&acc)[2][4][2
       for (int e = 0; e < 2; ++e) C[(c0 + j * 8 + 2 * t + e) * SC + r0 + i * 8 + g] = acc[i][j][e];
 }
 
+// Jacobi rotation of the 2x2 problem [[aii, aij], [aij, ajj]] (identity when r == 0):
+// t = sgn(theta) / (|theta| + sqrt(1 + theta^2)), theta = (ajj - aii) / (2 aij), written with one
+// square root and one division: t = 2 aij sgn(d) / (|d| + sqrt(d^2 + 4 aij^2))
+__device__ __forceinline__ void rotation(double aii, double ajj, double aij, int r, double& c, double& s, double& t) {
+  const double dd = ajj - aii, a2 = 2.0 * aij;
+  const double tt = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
+  const double cc = rsqrt(fma(tt, tt, 1.0));
+  t = r ? tt : 0.0;
+  c = r ? cc : 1.0;
+  s = r ? tt * cc : 0.0;
+}
+
+// n = R_P^T B R_Q for the 2x2 block B (rows of pair P, columns of pair Q), explicit fma order so
+// the owner warps and the look-ahead produce the same bits
+__device__ __forceinline__ void two_sided(double b00, double b01, double b10, double b11, double cp, double sp,
+                                          double c, double s, double (&n)[4]) {
+  const double m00 = fma(cp, b00, -(sp * b10)), m01 = fma(cp, b01, -(sp * b11));
+  const double m10 = fma(sp, b00, cp * b10), m11 = fma(sp, b01, cp * b11);
+  n[0] = fma(c, m00, -(s * m01));
+  n[1] = fma(s, m00, c * m01);
+  n[2] = fma(c, m10, -(s * m11));
+  n[3] = fma(s, m10, c * m11);
+}
+
 // One pair's local solve (block k of round p.round) by a CTA of NT threads (NT/32 warps; warp w
 // owns row pairs w, w + NT/32, ... and W rows w, w + NT/32, ...).  `sm` holds 3 PS x LS doubles.
 template <int NT>
@@ -222,29 +246,59 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
   }
   __syncthreads();
 
+  // Rotation table, double-buffered by step parity: (c, s, t, r) of the 32 pairs of a step,
+  // computed ONCE by warp 0 instead of redundantly by every warp (the FP64 pipe is shared with
+  // the DMMA products of the apply CTAs co-resident in the fused round).  Look-ahead: during
+  // step s warp 0 already forms the three entries of A_next each pair of step s+1 needs (the
+  // same 2x2 transforms the owner warps apply, so the same bits) and that pair's rotation, so
+  // a step still needs only its one closing barrier.
+  __shared__ double tab_c[2][32], tab_s[2][32], tab_t[2][32];
+  __shared__ int tab_r[2][32];
+  auto make_rot = [&](double aii, double ajj, double aij, int buf) {
+    const int r = needs_rotation_sq(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
+    double c, s, t;
+    rotation(aii, ajj, aij, r, c, s, t);
+    tab_c[buf][lane] = c;
+    tab_s[buf][lane] = s;
+    tab_t[buf][lane] = t;
+    tab_r[buf][lane] = r;
+  };
+  if (warp == 0) {
+    int a, b;
+    circle_pair(PS, 0, lane, a, b);
+    make_rot(Acur[a * LS + a], Acur[b * LS + b], Acur[a * LS + b], 0);
+  }
+  __syncthreads();
+  int cur = 0;
   for (int sweep = 0; sweep < p.max_local_sweeps; ++sweep) {
     int rotated = 0;
     for (int step = 0; step < PS - 1; ++step) {
-      // rotation of pair `lane` (computed redundantly by every warp: no broadcast, no barrier).
-      // Branch-free: non-rotating pairs carry (c, s, t) = (1, 0, 0), which leaves every entry
-      // bit-identical, so all 2x2 updates of a step are independent straight-line code the
-      // compiler can interleave (the former per-pair branches serialised them).
+      // rotation of pair `lane` from the table.  Branch-free: non-rotating pairs carry
+      // (c, s, t) = (1, 0, 0), which leaves every entry bit-identical.
       int a, b;
       circle_pair(PS, step, lane, a, b);
-      const double aii = Acur[a * LS + a], ajj = Acur[b * LS + b], aij = Acur[a * LS + b];
-      const int r = needs_rotation_sq(aij, aii, ajj, tr, tloc, p.keep_floor, p.tol_angle);
-      double c, s, t;
-      {
-        // t = sgn(theta) / (|theta| + sqrt(1 + theta^2)), theta = (ajj - aii) / (2 aij), written
-        // with one square root and one division: t = 2 aij sgn(d) / (|d| + sqrt(d^2 + 4 aij^2))
-        const double dd = ajj - aii, a2 = 2.0 * aij;
-        const double tt = (dd >= 0.0 ? a2 : -a2) / (fabs(dd) + sqrt(fma(dd, dd, a2 * a2)));
-        const double cc = rsqrt(fma(tt, tt, 1.0));
-        t = r ? tt : 0.0;
-        c = r ? cc : 1.0;
-        s = r ? tt * cc : 0.0;
-      }
+      const double c = tab_c[cur][lane], s = tab_s[cur][lane], t = tab_t[cur][lane];
+      const int r = tab_r[cur][lane];
       rotated |= r;
+      if (warp == 0) {
+        // look-ahead: pair `lane` of the next step is (x, y); x sits in pair kx of this step, y in ky
+        const int ns = step + 1 < PS - 1 ? step + 1 : 0;
+        int x, y, ax, bx, ay, by;
+        circle_pair(PS, ns, lane, x, y);
+        const int kx = pair_of(PS, step, x), ky = pair_of(PS, step, y);
+        circle_pair(PS, step, kx, ax, bx);
+        circle_pair(PS, step, ky, ay, by);
+        const double txx = tab_t[cur][kx], tyy = tab_t[cur][ky];
+        const double xx = x == ax ? fma(-txx, Acur[ax * LS + bx], Acur[ax * LS + ax])
+                                  : fma(txx, Acur[ax * LS + bx], Acur[bx * LS + bx]);
+        const double yy = y == ay ? fma(-tyy, Acur[ay * LS + by], Acur[ay * LS + ay])
+                                  : fma(tyy, Acur[ay * LS + by], Acur[by * LS + by]);
+        double n[4];
+        two_sided(Acur[ax * LS + ay], Acur[ax * LS + by], Acur[bx * LS + ay], Acur[bx * LS + by], tab_c[cur][kx],
+                  tab_s[cur][kx], tab_c[cur][ky], tab_s[cur][ky], n);
+        const double xy = x == ax ? (y == ay ? n[0] : n[1]) : (y == ay ? n[2] : n[3]);
+        make_rot(xx, yy, xy, cur ^ 1);
+      }
       // A_next = R^T A R : this warp owns row pairs P = warp + NW h, column pair Q = lane; all
       // operands are loaded before any store
       {
@@ -254,10 +308,9 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           const int P = warp + NW * h;
-          cps[h] = __shfl_sync(0xffffffffu, c, P);
-          sps[h] = __shfl_sync(0xffffffffu, s, P);
-          i1s[h] = __shfl_sync(0xffffffffu, a, P);
-          j1s[h] = __shfl_sync(0xffffffffu, b, P);
+          cps[h] = tab_c[cur][P];
+          sps[h] = tab_s[cur][P];
+          circle_pair(PS, step, P, i1s[h], j1s[h]);
         }
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
@@ -269,19 +322,16 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           const bool dg = (warp + NW * h) == lane;
-          const double cp = cps[h], sp = sps[h];
           const double b00 = v[h][0], b01 = v[h][1], b10 = v[h][2], b11 = v[h][3];
-          const double m00 = cp * b00 - sp * b10, m01 = cp * b01 - sp * b11;
-          const double m10 = sp * b00 + cp * b10, m11 = sp * b01 + cp * b11;
-          const double n00 = c * m00 - s * m01, n01 = s * m00 + c * m01;
-          const double n10 = c * m10 - s * m11, n11 = s * m10 + c * m11;
+          double n[4];
+          two_sided(b00, b01, b10, b11, cps[h], sps[h], c, s, n);
           // the pair's own 2x2 block (b00 = a_ii, b01 = b10 = a_ij, b11 = a_jj): exact annihilation
-          const double d00 = b00 - t * b01, d11 = b11 + t * b01, od = r ? 0.0 : b01;
+          const double d00 = fma(-t, b01, b00), d11 = fma(t, b01, b11), od = r ? 0.0 : b01;
           const int i1 = i1s[h], j1 = j1s[h];
-          Anx[i1 * LS + a] = dg ? d00 : n00;
-          Anx[i1 * LS + b] = dg ? od : n01;
-          Anx[j1 * LS + a] = dg ? od : n10;
-          Anx[j1 * LS + b] = dg ? d11 : n11;
+          Anx[i1 * LS + a] = dg ? d00 : n[0];
+          Anx[i1 * LS + b] = dg ? od : n[1];
+          Anx[j1 * LS + a] = dg ? od : n[2];
+          Anx[j1 * LS + b] = dg ? d11 : n[3];
         }
       }
       // W <- W R on this warp's rows (identity for non-rotating pairs)
@@ -303,6 +353,7 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
       double* tmp = Acur;
       Acur = Anx;
       Anx = tmp;
+      cur ^= 1;
       __syncthreads();
     }
     if (!__syncthreads_or(rotated)) break;
