@@ -521,7 +521,11 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
   int64_t splits = 1;
   if (!b_upper && pl.ntiles < target) {
     splits = target / std::max<int64_t>(pl.ntiles, 1);
-    splits = std::min<int64_t>(splits, std::max<int64_t>(K / 512, 1));  // >= 512 k per split
+    // >= 512 k per split; a GEMM of at most 16 output tiles (the deep levels of chol_inv_run, small
+    // node products) splits down to 64 k: one 128x128 tile contracts 16 k per ~2 us on its SM, so
+    // a single-tile GEMM with K = 256 was ~35 us of one SM's DMMA pipe
+    const int64_t min_k = pl.ntiles <= 16 ? 64 : 512;
+    splits = std::min<int64_t>(splits, std::max<int64_t>(K / min_k, 1));
     splits = std::min<int64_t>(splits, 64);
     splits = std::max<int64_t>(splits, 1);
   }
