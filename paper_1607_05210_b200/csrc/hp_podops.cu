@@ -262,44 +262,51 @@ __global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_
     L[i][j] = (i < kb && j < kb && i >= j) ? A[(k0 + j) * lda + k0 + i] : 0.0;
     X[i][j] = (i == j) ? 1.0 : 0.0;
   }
+  // pivot 0; every later pivot is taken by the thread that applied its last update (below)
+  if (tid == 0 && kb > 0) {
+    const double d0 = L[0][0];
+    if (!(d0 > 0.0)) {
+      bad = 1;
+      L[0][0] = 1.0;
+    } else {
+      L[0][0] = sqrt(d0);
+    }
+  }
   __syncthreads();
+  // One barrier per column: column j of L and row j of R = L^{-1} are scaled by 1 / L[j][j] on the
+  // fly where they are read (in place only at the write-back), so the products are the ones an
+  // in-place scaling would form -- same bits, no separate scaling phase.
   for (int j = 0; j < kb; ++j) {
-    if (tid == 0) {
-      const double dj = L[j][j];
-      if (!(dj > 0.0)) {
-        bad = 1;
-        L[j][j] = 1.0;
-      } else {
-        L[j][j] = sqrt(dj);
-      }
-    }
-    __syncthreads();
     const double rpiv = 1.0 / L[j][j];
-    if (tid < CB) {
-      if (tid > j && tid < kb) L[tid][j] *= rpiv;       // column j of L
-    } else if (tid - CB <= j) {
-      X[j][tid - CB] *= rpiv;                           // row j of L^{-1}: X[j][c] = R[j][c] / L[j][j]
-    }
-    __syncthreads();
-    // trailing A -= l_j l_j^T (lower part) and R[i][c] -= L[i][j] X[j][c] (i > j, c <= j):
+    // trailing A -= l_j l_j^T (lower part) and R[i][c] -= L[i][j] R[j][c] (i > j, c <= j):
     // thread = (column c, row phase), no index division
     {
       const int c = tid & (CB - 1);
-      const double xjc = X[j][c], lcj = L[c][j];
+      const double xjc = X[j][c] * rpiv, lcj = L[c][j] * rpiv;
       for (int ii = j + 1 + (tid >> 6); ii < kb; ii += 256 / CB) {
-        const double lij = L[ii][j];
+        const double lij = L[ii][j] * rpiv;
         if (c <= j)
           X[ii][c] -= lij * xjc;
         else if (c <= ii)
           L[ii][c] -= lij * lcj;
       }
     }
+    if (tid == j + 1 && j + 1 < kb) {  // this thread just applied the last update of the next pivot
+      const double dn = L[j + 1][j + 1];
+      if (!(dn > 0.0)) {
+        bad = 1;
+        L[j + 1][j + 1] = 1.0;
+      } else {
+        L[j + 1][j + 1] = sqrt(dn);
+      }
+    }
     __syncthreads();
   }
   for (int e = tid; e < kb * kb; e += 256) {
     const int j = e / kb, i = e % kb;
-    A[(k0 + j) * lda + k0 + i] = (i >= j) ? L[i][j] : 0.0;
-    Linv[(k0 + j) * ldi + k0 + i] = (i >= j) ? X[i][j] : 0.0;
+    const double li = i == j ? L[i][i] : L[i][j] * (1.0 / L[j][j]);
+    A[(k0 + j) * lda + k0 + i] = (i >= j) ? li : 0.0;
+    Linv[(k0 + j) * ldi + k0 + i] = (i >= j) ? X[i][j] * (1.0 / L[i][i]) : 0.0;
   }
   if (tid == 0 && bad) atomicOr(info, 1);
 }
