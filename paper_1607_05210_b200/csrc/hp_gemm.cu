@@ -526,7 +526,7 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
     // a single-tile GEMM with K = 256 was ~35 us of one SM's DMMA pipe
     const int64_t min_k = pl.ntiles <= 16 ? 64 : 512;
     splits = std::min<int64_t>(splits, std::max<int64_t>(K / min_k, 1));
-    splits = std::min<int64_t>(splits, 64);
+    splits = std::min<int64_t>(splits, target);  // a one-tile output over a long K (a chain merge's drift SYRK) spreads over the whole chip
     splits = std::max<int64_t>(splits, 1);
   }
   pl.kspan = ceil_div(ceil_div(K, splits), BK) * BK;
