@@ -49,6 +49,10 @@ typedef struct hp_vecset {
 int hp_abi_version(void);
 /* Number of kernels this library has launched in the process (monotonic). */
 long long hp_launch_count(void);
+/* Diagnostics (no reference counterpart; never changes a result): bit 0 prints one line per
+ * Jacobi sweep, bit 1 adds CUDA-event timing of one mid-sweep round, bit 2 times the CholQR
+ * factorisation.  Returns the previous flags.  The library reads no environment variables. */
+int hp_set_debug(int flags);
 const char* hp_last_error(void);
 int hp_device_sm_count(int device);
 
@@ -154,6 +158,14 @@ int hp_signs(double* U, int64_t ldu, int64_t d, int64_t N, double* R, int64_t ld
 int hp_gram_drift(const double* C, int64_t ldc, int64_t N, double* drift_out, void* stream);
 int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
                   int64_t* idx, void* stream);
+/* hp_add -- dst[i] += src[i], i < n (contiguous, device): the fixed-order binary-tree sum of the
+ *   row-distributed root's per-shard Gram partials (replaces the BLAS sum inside the reference's
+ *   one-GPU Gram, pod.py:208-211, when the root is split by rows). */
+int hp_add(double* dst, const double* src, int64_t n, void* stream);
+/* hp_col_norms_sq -- out[j] = sum_i w_i A(i,j)^2 (weights nullable = Euclidean): the reference's
+ *   InnerProductSpace.norms_sq (pod.py:93-97).  out: cols doubles (device). */
+int hp_col_norms_sq(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* weights, double* out,
+                    void* stream);
 size_t hp_chol_inverse_workspace_bytes(int64_t N);
 int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl, int* info_out, void* ws,
                     size_t ws_bytes, void* stream);

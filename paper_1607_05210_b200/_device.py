@@ -33,25 +33,23 @@ DRIFT_TOL = 1e-8          # pod.py:247
 JACOBI_TOL_REL = 2.0 ** -52
 JACOBI_TOL_ABS = 16 * 2.0 ** -52  # absolute off-diagonal trigger, x max|g_ii| (Gram rounding floor)
 JACOBI_MAX_SWEEPS = 60
-# eigensolver: "pcjacobi" = pivoted-Cholesky preconditioned block Jacobi (default),
-# "jacobi" = block Jacobi directly on the Gramian (kept for comparison)
-import os as _os
-EIG_METHOD = _os.environ.get("HP_EIG_METHOD", "pcjacobi")
-PSTRF_TOL = float(_os.environ.get("HP_PSTRF_TOL", str(2.0 ** -52)))  # stop pivoting at u * max|G_ii|
+# Eigensolver numerics.  Fixed constants of the product path: the library and this module read
+# no environment variables (a stray variable must never change a result).  Studies override
+# them explicitly in-process (tools/*.py), never through the environment.
+PSTRF_TOL = 2.0 ** -52  # stop pivoting at u * max|G_ii|
 # Rayleigh-Ritz polish of the preconditioned eigenpairs against G itself (restores LAPACK-class
 # accuracy of the eigenvalues at the Gram cutoff): eigenpairs with lambda above
 # POLISH_FACTOR * cutoff * lambda_max * m are re-solved in their own span.
-POLISH = _os.environ.get("HP_EIG_POLISH", "1") != "0"
 KEEP_SPECTRUM = False   # diagnostics: keep the last node's eigenvalues in LAST_SPECTRUM
 LAST_SPECTRUM: list = []
-POLISH_FACTOR = float(_os.environ.get("HP_EIG_POLISH_FACTOR", "1e-2"))
-PSTRF_POLISH_MARGIN = float(_os.environ.get("HP_PSTRF_POLISH_MARGIN", "0.25"))
-POLISH_TOL_REL = float(_os.environ.get("HP_EIG_POLISH_TOL_REL", str(2.0 ** -52)))
-POLISH_TOL_ABS = float(_os.environ.get("HP_EIG_POLISH_TOL_ABS", "1e-30"))
+POLISH_FACTOR = 1e-2
+PSTRF_POLISH_MARGIN = 0.25
+POLISH_TOL_REL = 2.0 ** -52
+POLISH_TOL_ABS = 1e-30
 # rotations whose angle |g_ij| / |g_jj - g_ii| is below this change no output digit
-POLISH_TOL_ANGLE = float(_os.environ.get("HP_EIG_POLISH_TOL_ANGLE", "1e-14"))
+POLISH_TOL_ANGLE = 1e-14
 # absolute trigger of the preconditioned (H = L^T L) phase; the polish carries the final accuracy
-PC_TOL_ABS = float(_os.environ.get("HP_PC_TOL_ABS", str(16 * 2.0 ** -52)))
+PC_TOL_ABS = 16 * 2.0 ** -52
 
 
 class Profiler:
@@ -194,7 +192,7 @@ _COPY_INFLIGHT: list = []   # completion events of the uploads queued on the cop
 # pinned memory) waits behind the copy engine's pending host-to-device work, so an unbounded queue
 # (all 16 leaves of config 1 request their 0.8 GB upload at once) stalls every leaf's first host
 # read-back for most of the 13 GB transfer; two in flight keep the DMA engine busy
-COPY_MAX_INFLIGHT = int(_os.environ.get("HP_COPY_MAX_INFLIGHT", "2"))
+COPY_MAX_INFLIGHT = 2
 
 
 def copy_stream():
@@ -354,6 +352,48 @@ def pack_parts(parts: list[Part]) -> list[Part]:
     return [Part(out, scale)]
 
 
+def _operand(x) -> tuple:
+    """(DevMat, was_host) for a d x k host array / torch tensor / DevMat operand."""
+    if isinstance(x, DevMat):
+        return x, False
+    host = not (torch.is_tensor(x) and x.is_cuda)
+    return upload(x, check_finite=False), host
+
+
+def space_gram(a, b, w_dev=None):
+    """InnerProductSpace.gram (pod.py:87-91) on the device: a^T (w * b) by the DMMA GEMM engine
+    (w scales b's rows first, as the reference forms w[:, None] * b).  Host inputs give a NumPy
+    result, device inputs a CUDA tensor."""
+    lib = N.load()
+    st = _stream()
+    A, ha = _operand(a)
+    B, hb = _operand(b)
+    if A.rows != B.rows:
+        raise ValueError(f"operands have {A.rows} and {B.rows} rows")
+    if w_dev is not None and B.cols:
+        Bw = DevMat.empty(B.rows, B.cols)
+        N.check(lib.hp_scale(B.ptr, B.ld, B.rows, B.cols, w_dev.data_ptr(), None, None, Bw.ptr, Bw.ld, st), "w * b")
+        B = Bw
+    C = DevMat.empty(A.cols, B.cols, zero=True)
+    if A.cols and B.cols and A.rows:
+        ws = _ws(lib.hp_gemm_workspace_bytes(A.cols, B.cols, A.rows, 0, 0))
+        N.check(lib.hp_gemm(1, 1, A.cols, B.cols, A.rows, A.vecset(), B.vecset(), 1.0, 0.0, C.ptr, C.ld, None, None,
+                            None, 0, 0, ws.data_ptr(), ws.numel(), st), "gram")
+    return C.to_numpy() if (ha and hb) else C.tensor()
+
+
+def space_norms_sq(a, w_dev=None):
+    """InnerProductSpace.norms_sq (pod.py:93-97) on the device: per column sum_i w_i a_i^2."""
+    lib = N.load()
+    A, host = _operand(a)
+    out = torch.zeros(max(A.cols, 1), dtype=torch.float64, device="cuda")
+    if A.cols:
+        N.check(lib.hp_col_norms_sq(A.ptr, A.ld, A.rows, A.cols, _ptr(w_dev), out.data_ptr(), _stream()),
+                "norms_sq")
+    out = out[: A.cols]
+    return out.cpu().numpy() if host else out
+
+
 def weigh_parts(parts: list[Part], sqrt_w) -> list[Part]:
     """Euclidean coordinates of weighted snapshots (InnerProductSpace.weigh, pod.py:76-80)."""
     lib = N.load()
@@ -413,7 +453,7 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
     return G, total, keep
 
 
-BJORCK_MAX_DRIFT = float(_os.environ.get("HP_BJORCK_MAX_DRIFT", "0.05"))  # Newton-Schulz: quadratic from here
+BJORCK_MAX_DRIFT = 0.05  # Newton-Schulz: quadratic from here
 
 
 def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
@@ -497,100 +537,95 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
     eigh(G) (pod.py:329), a handful of Jacobi sweeps instead of dozens."""
     lib = N.load()
     st = _stream()
-    Lf = None
-    basis, divide = None, False
-    if EIG_METHOD == "pcjacobi" and m > 0:
-        Lf = DevMat.empty(m, m)
-        piv = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
-        rank = ctypes.c_int64(0)
-        ws = _ws(lib.hp_pstrf_workspace_bytes(m))
-        with _phase("pstrf", float(m) ** 3 / 3.0):
-            # with the polish, pivots below a quarter of its floor (lambda <= POLISH_FACTOR * cutoff
-            # * lambda_max * m) only feed directions the subspace step damps anyway
-            tol_lam = PSTRF_POLISH_MARGIN * POLISH_FACTOR * float(cutoff) * m if POLISH else 0.0
-            N.check(lib.hp_pstrf(G.ptr, G.ld, m, Lf.ptr, Lf.ld, piv.data_ptr(), PSTRF_TOL, tol_lam,
-                                 ctypes.byref(rank), ws.data_ptr(), ws.numel(), st), "pivoted Cholesky")
+    if m == 0:
+        return EigVectors(0.0, 0, 0, 0.0, ones(0), None, 0)
+    Lf = DevMat.empty(m, m)
+    piv = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+    rank = ctypes.c_int64(0)
+    ws = _ws(lib.hp_pstrf_workspace_bytes(m))
+    with _phase("pstrf", float(m) ** 3 / 3.0):
+        # with the polish, pivots below a quarter of its floor (lambda <= POLISH_FACTOR * cutoff
+        # * lambda_max * m) only feed directions the subspace step damps anyway
+        tol_lam = PSTRF_POLISH_MARGIN * POLISH_FACTOR * float(cutoff) * m
+        N.check(lib.hp_pstrf(G.ptr, G.ld, m, Lf.ptr, Lf.ld, piv.data_ptr(), PSTRF_TOL, tol_lam,
+                             ctypes.byref(rank), ws.data_ptr(), ws.numel(), st), "pivoted Cholesky")
+    del ws
+    r = int(rank.value)
+    Lr = Lf.view_cols(0, r)
+    H = DevMat.empty(r, r)
+    if r:
+        ws = _ws(lib.hp_gram_workspace_bytes(m, r))
+        with _phase("gram", float(m) * r * (r + 1)):
+            N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
+                    "H = L^T L")
         del ws
-        r = int(rank.value)
-        Lr = Lf.view_cols(0, r)
-        H = DevMat.empty(r, r)
-        if r:
-            ws = _ws(lib.hp_gram_workspace_bytes(m, r))
-            with _phase("gram", float(m) * r * (r + 1)):
-                N.check(lib.hp_gram(Lr.vecset(), m, r, None, H.ptr, H.ld, ws.data_ptr(), ws.numel(), st),
-                        "H = L^T L")
-            del ws
-        # with the polish, H's eigenvalues only select K and scale Q0: no Rayleigh refinement
-        lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS if POLISH else None, refine=not POLISH)
-        nev = r
-        basis, divide = Lf, True
-        if POLISH and r:
-            # K = #{lambda_H >= POLISH_FACTOR * cutoff * lambda_max * m}; sig = sqrt(lambda_H[:K])
-            sig_h = torch.empty(r, dtype=torch.float64, device="cuda")
-            info_h = torch.empty(4, dtype=torch.float64, device="cuda")
-            N.check(lib.hp_truncate(lam.data_ptr(), r, 0.0, float(cutoff) * POLISH_FACTOR, m, sig_h.data_ptr(),
-                                    info_h.data_ptr(), st), "polish count")
-            info_hh = host_read(info_h[:2])
-            lam_max_h, K = float(info_hh[0]), int(info_hh[1])
-            if K:
-                # Q0 = L W_K Lambda_K^{-1/2}: approximate eigenvectors of G from the preconditioned solve.
-                # One subspace-iteration step X = G Q0 Lambda_K^{-1} damps the components along
-                # eigenvectors outside span(Q0) (left there by the Cholesky backward error) by
-                # lambda_j / lambda_i; CholQR keeps the descending order; Rayleigh-Ritz on
-                # G2 = X^T G X then resolves the mixing inside the span.
-                ws = _ws(max(lib.hp_gemm_workspace_bytes(m, K, r, 0, 0), lib.hp_gemm_workspace_bytes(m, K, m, 0, 0),
-                             lib.hp_gemm_workspace_bytes(K, K, m, 1, 0)))
-                Q0 = DevMat.empty(m, K)
-                with _phase("polish_q0", 2.0 * m * r * K):
-                    N.check(lib.hp_gemm(0, 1, m, K, r, Lr.vecset(), W.vecset(), 1.0, 0.0, Q0.ptr, Q0.ld, None, None,
-                                        sig_h.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "Q0 = L W / sigma")
-                X = DevMat.empty(m, K)
-                with _phase("polish_x", 2.0 * m * m * K):
-                    N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), Q0.vecset(), 1.0, 0.0, X.ptr, X.ld, None, None,
-                                        lam.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "X = G Q0 / lambda")
-                del Q0
-                ph = _phase("polish_orth", 0.0)
-                with ph:
-                    # any orthonormal basis of span(X) serves Rayleigh-Ritz: Bjorck / Newton-Schulz steps
-                    # X <- X (3 I - X^T X) / 2 (two DMMA GEMMs each, no sequential factorisation) while
-                    # the drift is small, CholQR otherwise
-                    drift_x = None
-                    # the trailing columns of X (eigenpairs near the polish floor, where Q0 is least
-                    # accurate) can be numerically dependent; CholQR keeps nested spans, so on a
-                    # breakdown the basis is shortened from the tail -- never below the eigenpairs
-                    # above the Gram cutoff plus half the margin -- and orthonormalised again
-                    k_cut = int(host_read((lam[:K] >= float(cutoff) * lam_max_h * m).sum())[0])
-                    k_min = min(K, k_cut + max(1, (K - k_cut) // 2))
-                    while drift_x is None:
-                        try:
-                            drift_x = _orthonormalise_basis(X, ws, st, ph)
-                        except np.linalg.LinAlgError:
-                            if K <= k_min:
-                                raise
-                            K = max(k_min, K - max(1, (K - k_cut) // 4))
-                            X = X.view_cols(0, K)
-                T = DevMat.empty(m, K)
-                G2 = DevMat.empty(K, K)
-                with _phase("polish_rr", 2.0 * m * m * K + float(m) * K * (K + 1)):
-                    N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), X.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None,
-                                        None, 0, 0, ws.data_ptr(), ws.numel(), st), "T = G X")
-                    N.check(lib.hp_gemm(1, 1, K, K, m, X.vecset(), T.vecset(), 1.0, 0.0, G2.ptr, G2.ld, None, None,
-                                        None, 1, 0, ws.data_ptr(), ws.numel(), st), "G2 = X^T G X")
-                del T, ws
-                # G2 is nearly diagonal and graded: relative criterion, but never rotate two
-                # eigenvalues that are both below a tenth of the Gram cutoff (pod.py:284)
-                floor = 0.1 * float(cutoff) * lam_max_h * m
-                lam, W, sweeps2 = _syev(G2, K, st, "eigensolve_polish", tol_rel=POLISH_TOL_REL,
-                                        tol_abs=POLISH_TOL_ABS, keep_floor=floor, tol_angle=POLISH_TOL_ANGLE)
-                sweeps += sweeps2
-                nev = K
-                basis, divide = X, False
-                del G2, Lf
-                Lf = None
-    else:
-        lam, W, sweeps = _syev(G, m, st)
-        nev = m
-        basis, divide = None, False
+    # with the polish, H's eigenvalues only select K and scale Q0: no Rayleigh refinement
+    lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS, refine=False)
+    nev = r
+    basis, divide = Lf, True
+    if r:
+        # K = #{lambda_H >= POLISH_FACTOR * cutoff * lambda_max * m}; sig = sqrt(lambda_H[:K])
+        sig_h = torch.empty(r, dtype=torch.float64, device="cuda")
+        info_h = torch.empty(4, dtype=torch.float64, device="cuda")
+        N.check(lib.hp_truncate(lam.data_ptr(), r, 0.0, float(cutoff) * POLISH_FACTOR, m, sig_h.data_ptr(),
+                                info_h.data_ptr(), st), "polish count")
+        info_hh = host_read(info_h[:2])
+        lam_max_h, K = float(info_hh[0]), int(info_hh[1])
+        if K:
+            # Q0 = L W_K Lambda_K^{-1/2}: approximate eigenvectors of G from the preconditioned solve.
+            # One subspace-iteration step X = G Q0 Lambda_K^{-1} damps the components along
+            # eigenvectors outside span(Q0) (left there by the Cholesky backward error) by
+            # lambda_j / lambda_i; CholQR keeps the descending order; Rayleigh-Ritz on
+            # G2 = X^T G X then resolves the mixing inside the span.
+            ws = _ws(max(lib.hp_gemm_workspace_bytes(m, K, r, 0, 0), lib.hp_gemm_workspace_bytes(m, K, m, 0, 0),
+                         lib.hp_gemm_workspace_bytes(K, K, m, 1, 0)))
+            Q0 = DevMat.empty(m, K)
+            with _phase("polish_q0", 2.0 * m * r * K):
+                N.check(lib.hp_gemm(0, 1, m, K, r, Lr.vecset(), W.vecset(), 1.0, 0.0, Q0.ptr, Q0.ld, None, None,
+                                    sig_h.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "Q0 = L W / sigma")
+            X = DevMat.empty(m, K)
+            with _phase("polish_x", 2.0 * m * m * K):
+                N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), Q0.vecset(), 1.0, 0.0, X.ptr, X.ld, None, None,
+                                    lam.data_ptr(), 0, 0, ws.data_ptr(), ws.numel(), st), "X = G Q0 / lambda")
+            del Q0
+            ph = _phase("polish_orth", 0.0)
+            with ph:
+                # any orthonormal basis of span(X) serves Rayleigh-Ritz: Bjorck / Newton-Schulz steps
+                # X <- X (3 I - X^T X) / 2 (two DMMA GEMMs each, no sequential factorisation) while
+                # the drift is small, CholQR otherwise
+                drift_x = None
+                # the trailing columns of X (eigenpairs near the polish floor, where Q0 is least
+                # accurate) can be numerically dependent; CholQR keeps nested spans, so on a
+                # breakdown the basis is shortened from the tail -- never below the eigenpairs
+                # above the Gram cutoff plus half the margin -- and orthonormalised again
+                k_cut = int(host_read((lam[:K] >= float(cutoff) * lam_max_h * m).sum())[0])
+                k_min = min(K, k_cut + max(1, (K - k_cut) // 2))
+                while drift_x is None:
+                    try:
+                        drift_x = _orthonormalise_basis(X, ws, st, ph)
+                    except np.linalg.LinAlgError:
+                        if K <= k_min:
+                            raise
+                        K = max(k_min, K - max(1, (K - k_cut) // 4))
+                        X = X.view_cols(0, K)
+            T = DevMat.empty(m, K)
+            G2 = DevMat.empty(K, K)
+            with _phase("polish_rr", 2.0 * m * m * K + float(m) * K * (K + 1)):
+                N.check(lib.hp_gemm(0, 1, m, K, m, G.vecset(), X.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None,
+                                    None, 0, 0, ws.data_ptr(), ws.numel(), st), "T = G X")
+                N.check(lib.hp_gemm(1, 1, K, K, m, X.vecset(), T.vecset(), 1.0, 0.0, G2.ptr, G2.ld, None, None,
+                                    None, 1, 0, ws.data_ptr(), ws.numel(), st), "G2 = X^T G X")
+            del T, ws
+            # G2 is nearly diagonal and graded: relative criterion, but never rotate two
+            # eigenvalues that are both below a tenth of the Gram cutoff (pod.py:284)
+            floor = 0.1 * float(cutoff) * lam_max_h * m
+            lam, W, sweeps2 = _syev(G2, K, st, "eigensolve_polish", tol_rel=POLISH_TOL_REL,
+                                    tol_abs=POLISH_TOL_ABS, keep_floor=floor, tol_angle=POLISH_TOL_ANGLE)
+            sweeps += sweeps2
+            nev = K
+            basis, divide = X, False
+            del G2, Lf
+            Lf = None
     sig = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
     info = torch.empty(4, dtype=torch.float64, device="cuda")
     with _phase("truncate"):

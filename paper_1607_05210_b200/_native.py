@@ -32,6 +32,7 @@ class VecSet(ctypes.Structure):
 _SIGNATURES = {
     "hp_abi_version": (c_int, []),
     "hp_launch_count": (ctypes.c_longlong, []),
+    "hp_set_debug": (ctypes.c_int, [ctypes.c_int]),
     "hp_last_error": (ctypes.c_char_p, []),
     "hp_device_sm_count": (c_int, [c_int]),
     "hp_gemm_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_int, c_int]),
@@ -62,6 +63,8 @@ _SIGNATURES = {
     "hp_read_small": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "hp_add_diag": (c_int, [c_vp, c_i64, c_i64, c_dbl, c_vp]),
     "hp_gram_drift": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "hp_add": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "hp_col_norms_sq": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "hp_col_absmax": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "hp_chol_inverse_workspace_bytes": (c_size, [c_i64]),
     "hp_chol_inverse": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_size, c_vp]),

@@ -16,6 +16,8 @@ namespace hp {
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static std::atomic<int> g_debug{0};
+int debug_flags() { return g_debug.load(std::memory_order_relaxed); }
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
@@ -53,6 +55,9 @@ int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const 
 int finite_check_run(const double* src, int64_t lds, int64_t rows, int64_t cols, int* bad, cudaStream_t st);
 int sumsq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, double* out, double* partial,
               cudaStream_t st);
+int add_run(double* dst, const double* src, int64_t n, cudaStream_t st);
+int col_norms_sq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* w, double* out,
+                     cudaStream_t st);
 int col_absmax_run(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
                    int64_t* idx, cudaStream_t st);
 size_t pstrf_workspace_bytes(int64_t m);
@@ -165,6 +170,7 @@ extern "C" {
 
 int hp_abi_version(void) { return HP_ABI_VERSION; }
 long long hp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+int hp_set_debug(int flags) { return g_debug.exchange(flags); }
 const char* hp_last_error(void) { return hp::last_error(); }
 
 int hp_device_sm_count(int device) {
@@ -284,36 +290,45 @@ int hp_reorthonormalize(double* U, int64_t ldu, int64_t d, int64_t N, double* C,
   double* htrace = reinterpret_cast<double*>(pin + 80);
   int rc = HP_OK;
   int passes = 0;
-  // keep a copy of C in case the first factorisation fails
-  rc = scale_run(C, ldc, N, N, nullptr, nullptr, nullptr, A, ldn, st);
-  if (!rc) rc = cholqr_pass(U, ldu, d, N, C, ldc, X, ldx, L, base, ws_bytes, st, &hinfo[0]);
-  if (!rc) {
+  // stream sync + the Cholesky breakdown flag of the pass just queued (flag may be null)
+  auto sync_checked = [&](const int* flag, const char* what) -> int {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       set_error(std::string("reortho: ") + cudaGetErrorString(e));
-      rc = HP_ECUDA;
+      return HP_ECUDA;
     }
-  }
+    if (flag && *flag != 0) {
+      set_error(std::string("reortho: ") + what);
+      return HP_ELINALG;
+    }
+    return HP_OK;
+  };
+  // keep a copy of C in case the first factorisation fails
+  rc = scale_run(C, ldc, N, N, nullptr, nullptr, nullptr, A, ldn, st);
+  if (!rc) rc = cholqr_pass(U, ldu, d, N, C, ldc, X, ldx, L, base, ws_bytes, st, &hinfo[0]);
+  if (!rc) rc = sync_checked(nullptr, "");
   if (!rc && hinfo[0] != 0) {
     // shifted CholQR (Fukaya et al.): s = 11 (d N + N (N+1)) u ||U||_2^2, ||U||_2^2 <= trace(U^T U)
     trace_kernel<<<1, 256, 0, st>>>(A, ldn, N, C);
-    d2h_small(htrace, C, sizeof(double), st);
-    cudaStreamSynchronize(st);
+    HP_CHECK_LAUNCH("trace_kernel");
+    HP_CHECK_CUDA(d2h_small(htrace, C, sizeof(double), st));
+    rc = sync_checked(nullptr, "");
+    if (rc) return rc;
     const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * 1.1102230246251565e-16 * htrace[0];
     add_diag<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(A, ldn, N, shift);
+    HP_CHECK_LAUNCH("add_diag");
     rc = cholqr_pass(U, ldu, d, N, A, ldn, X, ldx, L, base, ws_bytes, st, &hinfo[1]);
-    if (!rc) {
-      cudaStreamSynchronize(st);
-      if (hinfo[1] != 0) {
-        set_error("reortho: shifted Cholesky broke down (modes numerically rank deficient)");
-        rc = HP_ELINALG;
-      }
-    }
-    // bring the shifted result back into U, then two plain passes follow
+    if (!rc) rc = sync_checked(&hinfo[1], "shifted Cholesky broke down (modes numerically rank deficient)");
+    // bring the shifted result back into U, then a plain pass (checked here) and the second pass
     if (!rc) rc = scale_run(X, ldx, d, N, nullptr, nullptr, nullptr, U, ldu, st);
     if (!rc) rc = gram_sym(U, ldu, d, N, A, ldn, gws, gwsb, st);
     if (!rc) rc = cholqr_pass(U, ldu, d, N, A, ldn, X, ldx, L, base, ws_bytes, st, &hinfo[0]);
+    if (!rc) rc = sync_checked(&hinfo[0], "Cholesky after the shifted pass broke down");
     passes += 1;
+    if (rc) {
+      if (passes_out) *passes_out = passes;
+      return rc;
+    }
   }
   passes += 1;
   const bool single = (passes == 1) && (drift >= 0.0) && (drift <= kSinglePassDrift);
@@ -398,6 +413,17 @@ int hp_col_absmax(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t
   return col_absmax_run(U, ldu, rows, N, row_offset, vals, idx, (cudaStream_t)stream);
 }
 
+int hp_add(double* dst, const double* src, int64_t n, void* stream) {
+  HP_REQUIRE(n >= 0, "hp_add: negative length");
+  return add_run(dst, src, n, (cudaStream_t)stream);
+}
+
+int hp_col_norms_sq(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* weights, double* out,
+                    void* stream) {
+  HP_REQUIRE(rows >= 0 && cols >= 0 && lda >= std::max<int64_t>(rows, 1), "hp_col_norms_sq: bad dimensions");
+  return col_norms_sq_run(A, lda, rows, cols, weights, out, (cudaStream_t)stream);
+}
+
 static size_t tbytes(int64_t N) {
   return (size_t)((std::max<int64_t>(N, 1) + 1) & ~int64_t(1)) * chol_t_cols(N) * 8;
 }
@@ -420,7 +446,7 @@ int hp_chol_inverse(double* C, int64_t ldc, int64_t N, double* Linv, int64_t ldl
   int* info = reinterpret_cast<int*>(base + al(tbytes(N)));
   char* gws = base + al(tbytes(N)) + al(16);
   const size_t gwsb = ws_bytes - (size_t)(gws - base);
-  static const bool trace = getenv("HP_TRACE_CHOL") != nullptr;
+  const bool trace = (debug_flags() & DBG_CHOL_TRACE) != 0;
   cudaEvent_t ev[3];
   if (trace)
     for (auto& e : ev) cudaEventCreate(&e);

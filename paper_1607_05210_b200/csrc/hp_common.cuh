@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #include "hapod_b200.h"
@@ -129,6 +131,28 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int num_sms();
+
+// Diagnostics switched on through the C-ABI (hp_set_debug), never through the environment:
+// they only add CUDA-event timing printouts and never change a result.
+enum DebugFlags { DBG_JACOBI_TRACE = 1, DBG_JACOBI_ROUND_TIMING = 2, DBG_CHOL_TRACE = 4 };
+int debug_flags();
+
+// One-time per-DEVICE setup of kernel attributes (cudaFuncSetAttribute applies to the current
+// device only): each call site owns a bitmask of the devices it has configured; concurrent stream
+// workers and multi-GPU processes race-free.
+template <class F>
+int once_per_device(std::atomic<unsigned long long>& mask, F&& setup) {
+  int dev = 0;
+  HP_CHECK_CUDA(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return HP_OK;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (mask.load(std::memory_order_relaxed) & bit) return HP_OK;
+  const int rc = setup();
+  if (rc == HP_OK) mask.fetch_or(bit, std::memory_order_release);
+  return rc;
+}
 // Pinned host scratch of the calling host thread (allocated once, never freed per call: a
 // cudaFreeHost per call would synchronise the whole device and serialise concurrent node
 // streams).  Slots: [0, 64) Jacobi sweep counters, [64, 128) re-orthonormalisation flags.

@@ -539,12 +539,13 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
 template <bool AK, bool BKM, bool VEC>
 int launch_t(const Params& p, cudaStream_t st) {
   using L = Layout<AK, BKM>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};
+  int rc0 = once_per_device(configured, []() -> int {
     HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_kernel<AK, BKM, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        L::SMEM_BYTES));
-    configured = true;
-  }
+    return (int)HP_OK;
+  });
+  if (rc0 != HP_OK) return rc0;
   dim3 grid((unsigned)p.ntiles, 1, (unsigned)p.splits);
   gemm_kernel<AK, BKM, VEC><<<grid, THREADS, L::SMEM_BYTES, st>>>(p);
   HP_CHECK_LAUNCH("gemm_kernel");
@@ -583,7 +584,7 @@ bool encode_map(CUtensorMap* map, const double* base, int64_t inner, int64_t out
 template <bool AK, bool BKM>
 int launch_tma(const Params& p, cudaStream_t st, bool& done) {
   done = false;
-  static bool configured = false;
+  static std::atomic<unsigned long long> configured{0};
   TmaParams tp;
   tp.p = p;
   // K-major: inner = K (contiguous k of each vector), outer = M / N vectors, box {16, 128}
@@ -593,11 +594,12 @@ int launch_tma(const Params& p, cudaStream_t st, bool& done) {
   const bool ok_b = BKM ? encode_map(&tp.tb, p.B.base, p.K, p.N, p.B.ld, BK, BN)
                         : encode_map(&tp.tb, p.B.base, p.N, p.K, p.B.ld, 16, BK);
   if (!ok_a || !ok_b) return HP_OK;  // not encodable: caller uses the cp.async kernel
-  if (!configured) {
+  const int rc0 = once_per_device(configured, []() -> int {
     HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        TMA_SMEM));
-    configured = true;
-  }
+    return (int)HP_OK;
+  });
+  if (rc0 != HP_OK) return rc0;
   dim3 grid((unsigned)p.ntiles, 1, (unsigned)p.splits);
   gemm_tma_kernel<AK, BKM><<<grid, TTHREADS, TMA_SMEM, st>>>(tp);
   HP_CHECK_LAUNCH("gemm_tma_kernel");
@@ -614,7 +616,6 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   using namespace gemm;
   HP_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: negative dimension");
   HP_REQUIRE(!sym || M == N, "gemm: symmetric output needs M == N");
-  HP_REQUIRE(!(a_kmajor == false && b_kmajor == false) || true, "");
   if (M == 0 || N == 0) return HP_OK;
   Params p{};
   Plan pl = make_plan(M, N, K, sym, b_upper);
@@ -647,10 +648,9 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
     }
   }
   int rc;
-  static const bool use_tma = !(getenv("HP_GEMM_TMA") && atoi(getenv("HP_GEMM_TMA")) == 0);
   bool done = false;
   rc = HP_OK;
-  if (aligned16 && use_tma && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31)) {
+  if (aligned16 && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31)) {
     if (a_kmajor && b_kmajor)
       rc = launch_tma<true, true>(p, st, done);
     else if (!a_kmajor && b_kmajor)

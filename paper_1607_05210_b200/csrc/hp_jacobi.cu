@@ -5,7 +5,7 @@
 // columns of width 32.  A sweep is nb-1 rounds of a round-robin tournament;
 // in each round the nb/2 disjoint block pairs (p,q) are processed at once:
 //
-//   jac_local : one CTA per pair loads the 64x64 sub-problem G[I,I],
+//   local solve (first CTAs of jac_round): one CTA per pair loads the 64x64 sub-problem G[I,I],
 //               I = block p U block q, into shared memory.  If any off-diagonal
 //               entry exceeds tol_abs * max|g_ii| it diagonalises the copy with
 //               cyclic parallel-order Jacobi (32 disjoint rotations per step,
@@ -48,7 +48,6 @@ namespace jac {
 constexpr int BW = 32;        // block width
 constexpr int PS = 2 * BW;    // local problem size
 constexpr int LS = PS + 1;    // local smem stride
-constexpr int LT = 512;       // local solver threads
 constexpr int TS = PS + 4;    // apply-kernel smem stride (= 4 mod 16: conflict-free DMMA fragments)
 constexpr int AT = 256;       // apply threads
 
@@ -407,11 +406,6 @@ __device__ __forceinline__ void local_solve(const Params& p, int k, double* sm) 
     p.flags[k] = 1;
     atomicAdd(p.counter, 1);
   }
-}
-
-__global__ void __launch_bounds__(LT) jac_local(Params p) {
-  extern __shared__ double sm[];
-  local_solve<LT>(p, blockIdx.x, sm);
 }
 
 // async 16-byte copies: a 64x64 column-major W (contiguous) into smem stride TS
@@ -778,18 +772,16 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   // solves hidden under the apply of the fused round, so two local sweeps buy fewer outer sweeps
   // (root H phase 820 -> 778 ms); small problems (leaves, merges) and the nearly diagonal polish
   // (keep_floor > 0, few active pairs) have the local solve on the critical path: one sweep.
-  static const int local_sweeps_env = getenv("HP_JACOBI_LOCAL_SWEEPS") ? atoi(getenv("HP_JACOBI_LOCAL_SWEEPS")) : 0;
-  p.max_local_sweeps = local_sweeps_env > 0 ? local_sweeps_env : ((layout(n).nb / 2 >= 32 && keep_floor <= 0.0) ? 2 : 1);
+  p.max_local_sweeps = (layout(n).nb / 2 >= 32 && keep_floor <= 0.0) ? 2 : 1;
 
-  static bool configured = false;
-  const int local_smem = 3 * PS * LS * 8;
+  static std::atomic<unsigned long long> configured{0};
   const int apply_smem = 3 * PS * TS * 8;
-  if (!configured) {
-    HP_CHECK_CUDA(cudaFuncSetAttribute(jac_local, cudaFuncAttributeMaxDynamicSharedMemorySize, local_smem));
+  const int rc0 = once_per_device(configured, [&]() -> int {
     HP_CHECK_CUDA(cudaFuncSetAttribute(jac_round, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem));
     HP_CHECK_CUDA(cudaFuncSetAttribute(jac_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem));
-    configured = true;
-  }
+    return (int)HP_OK;
+  });
+  if (rc0 != HP_OK) return rc0;
   const int64_t npn = L.np * L.np;
   pad_copy<<<(unsigned)ceil_div(npn, 256), 256, 0, st>>>(G, ldg, n, p.G, p.V, L.np);
   HP_CHECK_LAUNCH("pad_copy");
@@ -810,11 +802,11 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   double prev_off = INFINITY;
   unsigned long long mm_total = 0;
   const double floor_ratio = 512.0 * 2.220446049250313e-16;
-  static const int trace = getenv("HP_JACOBI_TRACE") ? atoi(getenv("HP_JACOBI_TRACE")) : 0;
+  const int dbg = debug_flags();
+  const int trace = (dbg & DBG_JACOBI_ROUND_TIMING) ? 2 : (dbg & DBG_JACOBI_TRACE) ? 1 : 0;
   cudaEvent_t ev[3];
   if (trace > 1)
     for (auto& e : ev) cudaEventCreate(&e);
-  static const bool use_fused = !(getenv("HP_JACOBI_FUSED") && atoi(getenv("HP_JACOBI_FUSED")) == 0);
   HP_CHECK_CUDA(zero_async(p.tile_mark, (size_t)npairs * (npairs + 1) / 2 * 4, st));
   const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, 2 * (int64_t)nsm);  // one task per CTA (2 per SM)
   // small problems (leaves, merges) get a grid sized to their work -- about four apply tasks per
@@ -837,28 +829,18 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
       q.stamp = stamp + r + 1;
       return q;
     };
-    if (use_fused) {
-      jac_round<<<npairs, AT, apply_smem, st>>>(round_params(0), round_params(0), 1, 0);
-    } else {
-      jac_local<<<npairs, LT, local_smem, st>>>(round_params(0));
-    }
+    jac_round<<<npairs, AT, apply_smem, st>>>(round_params(0), round_params(0), 1, 0);
+    count_launches(1);
     for (int r = 0; r < R; ++r) {
       Params q = round_params(r);
       q.phase = 1;
       jac_apply<<<needed_grid, AT, apply_smem, st>>>(q);
       if (trace > 1 && r == R / 2) cudaEventRecord(ev[0], st);
       q.phase = 2;
-      if (use_fused) {
-        jac_round<<<rest_grid, AT, apply_smem, st>>>(q, round_params(r + 1 < R ? r + 1 : 0), r + 1 < R, 1);
-        count_launches(2);
-      } else {
-        jac_apply<<<rest_grid, AT, apply_smem, st>>>(q);
-        if (trace > 1 && r == R / 2) cudaEventRecord(ev[1], st);
-        if (r + 1 < R) jac_local<<<npairs, LT, local_smem, st>>>(round_params(r + 1));
-        count_launches(3);
-      }
+      jac_round<<<rest_grid, AT, apply_smem, st>>>(q, round_params(r + 1 < R ? r + 1 : 0), r + 1 < R, 1);
+      count_launches(2);
       if (trace > 1 && r == R / 2) {
-        if (use_fused) cudaEventRecord(ev[1], st);
+        cudaEventRecord(ev[1], st);
         cudaEventRecord(ev[2], st);
       }
     }

@@ -21,14 +21,49 @@ int scale_run(const double* src, int64_t lds, int64_t rows, int64_t cols, const 
 
 // ------------------------------------------------------------------ K3 truncation
 // info[0] = lam_max, info[1] = nkeep, info[2] = N, info[3] = tail_energy
-constexpr int TR_T = 1024;
+//
+// Bit-for-bit the reference's arithmetic (pod.py:198-205, 284-289):
+//   keep  = lam >= cutoff * lam_max * m                       (a prefix: lam is descending)
+//   sig   = sqrt(lam_keep)
+//   tails = reversed sequential cumsum of sig*sig (np.cumsum: one add per entry, smallest first;
+//           sig*sig rounded before the add -- no FMA contraction)
+//   N     = first index with tails[N] <= eps^2                 (np.argmax of the mask)
+//   tail  = np.sum(lam_keep[N:])                              (NumPy's pairwise summation)
+// The cumsum is inherently sequential; it runs on one thread from the smallest kept value
+// upward and stops as soon as the running tail exceeds eps^2 (rounding is monotone, so no
+// later index can satisfy the budget again) -- it only walks the discarded tail.
+constexpr int TR_T = 256;
+
+// numpy/_core/src/umath/loops_utils.h.src pairwise_sum (PW_BLOCKSIZE 128, 8-way unroll), the
+// summation np.sum applies to a contiguous float64 array.
+__device__ double np_pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+}
 
 __global__ void __launch_bounds__(TR_T) truncate_kernel(const double* lam, int64_t n, double eps, double cutoff,
                                                         int64_t m, double* sigma, double* info) {
-  __shared__ double chunk_tot[TR_T];
-  __shared__ double chunk_off[TR_T];
-  __shared__ int64_t sh_nkeep, sh_N;
-  __shared__ double red[TR_T];
+  __shared__ unsigned long long sh_nkeep;
   const int tid = threadIdx.x;
   const double lam_max = n > 0 ? lam[0] : 0.0;
   if (!(lam_max > 0.0)) {
@@ -40,65 +75,31 @@ __global__ void __launch_bounds__(TR_T) truncate_kernel(const double* lam, int64
     }
     return;
   }
-  const double thr = cutoff * lam_max * (double)m;
-  if (tid == 0) {
-    sh_nkeep = 0;
-    sh_N = n;  // placeholder
-  }
+  const double thr = __dmul_rn(__dmul_rn(cutoff, lam_max), (double)m);
+  if (tid == 0) sh_nkeep = 0;
   __syncthreads();
-  // keep = lam >= thr  (a prefix, lam sorted descending)
-  int64_t local_cnt = 0;
+  unsigned long long local_cnt = 0;
   for (int64_t i = tid; i < n; i += TR_T) local_cnt += (lam[i] >= thr);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&sh_nkeep), (unsigned long long)local_cnt);
+  atomicAdd(&sh_nkeep, local_cnt);
   __syncthreads();
-  const int64_t nk = sh_nkeep;
-  for (int64_t i = tid; i < nk; i += TR_T) sigma[i] = sqrt(lam[i]);
-  // tails[k] = sum_{i>=k} sigma_i^2, accumulated from the smallest upward within
-  // contiguous chunks, chunk offsets accumulated from the last chunk backward
-  const int64_t cs = (nk + TR_T - 1) / TR_T;
-  const int64_t b = (int64_t)tid * cs, e = min(nk, b + cs);
-  double s = 0.0;
-  for (int64_t i = e - 1; i >= b; --i) {
-    const double si = sqrt(lam[i]);
-    s += si * si;
+  const int64_t nk = (int64_t)sh_nkeep;
+  for (int64_t i = tid; i < nk; i += TR_T) sigma[i] = __dsqrt_rn(lam[i]);
+  if (tid != 0) return;
+  const double eps2 = __dmul_rn(eps, eps);
+  int64_t N = nk;  // tails[nk] = 0 always satisfies the budget
+  double run = 0.0;
+  for (int64_t i = nk - 1; i >= 0; --i) {
+    const double si = __dsqrt_rn(lam[i]);
+    run = __dadd_rn(run, __dmul_rn(si, si));
+    if (run <= eps2)
+      N = i;
+    else
+      break;
   }
-  chunk_tot[tid] = s;
-  __syncthreads();
-  if (tid == 0) {
-    double acc = 0.0;
-    for (int c = TR_T - 1; c >= 0; --c) {
-      chunk_off[c] = acc;
-      acc += chunk_tot[c];
-    }
-    sh_N = nk;  // tails[nk] = 0 always satisfies the budget
-  }
-  __syncthreads();
-  const double eps2 = eps * eps;
-  double run = chunk_off[tid];
-  int64_t first = nk;
-  for (int64_t i = e - 1; i >= b; --i) {
-    const double si = sqrt(lam[i]);
-    run += si * si;
-    if (run <= eps2) first = i;  // tails are non-increasing in i: keep the smallest index
-  }
-  if (first < nk) atomicMin(reinterpret_cast<unsigned long long*>(&sh_N), (unsigned long long)first);
-  __syncthreads();
-  const int64_t N = sh_N;
-  // tail energy = sum lam[N:nk]
-  double t = 0.0;
-  for (int64_t i = N + tid; i < nk; i += TR_T) t += lam[i];
-  red[tid] = t;
-  __syncthreads();
-  for (int st = TR_T / 2; st > 0; st >>= 1) {
-    if (tid < st) red[tid] += red[tid + st];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    info[0] = lam_max;
-    info[1] = (double)nk;
-    info[2] = (double)N;
-    info[3] = red[0];
-  }
+  info[0] = lam_max;
+  info[1] = (double)nk;
+  info[2] = (double)N;
+  info[3] = np_pairwise_sum(lam + N, nk - N);
 }
 
 int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
@@ -243,6 +244,47 @@ __global__ void col_absmax_kernel(const double* U, int64_t ldu, int64_t rows, in
   }
 }
 
+// per column: sum_i w_i a_i^2 (w nullable = Euclidean), fixed-order block reduction
+// (InnerProductSpace.norms_sq, pod.py:93-97)
+__global__ void col_norms_sq_kernel(const double* A, int64_t lda, int64_t rows, const double* w, double* out) {
+  __shared__ double red[256];
+  const double* col = A + (int64_t)blockIdx.x * lda;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += 256) {
+    const double a = col[i];
+    s += w ? a * (w[i] * a) : a * a;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
+int col_norms_sq_run(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* w, double* out,
+                     cudaStream_t st) {
+  if (cols == 0) return HP_OK;
+  col_norms_sq_kernel<<<(unsigned)cols, 256, 0, st>>>(A, lda, rows, w, out);
+  HP_CHECK_LAUNCH("col_norms_sq_kernel");
+  return HP_OK;
+}
+
+// dst <- dst + src (contiguous; the fixed-tree shard sums of the row-distributed root)
+__global__ void add_kernel(double* dst, const double* src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __dadd_rn(dst[i], src[i]);
+}
+
+int add_run(double* dst, const double* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return HP_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * 148);
+  add_kernel<<<grid, 256, 0, st>>>(dst, src, n);
+  HP_CHECK_LAUNCH("add_kernel");
+  return HP_OK;
+}
+
 int col_absmax_run(const double* U, int64_t ldu, int64_t rows, int64_t N, int64_t row_offset, double* vals,
                    int64_t* idx, cudaStream_t st) {
   if (N == 0) return HP_OK;
@@ -340,12 +382,13 @@ __global__ void __launch_bounds__(256) potrf_diag(double* A, int64_t lda, int64_
 static int chol_inv_rec(double* A, int64_t lda, int64_t o, int64_t n, double* Linv, int64_t ldi, double* T,
                         int64_t ldt, int* info, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n <= CB) {
-    static bool configured = false;
+    static std::atomic<unsigned long long> configured{0};
     const int pd_smem = 2 * CB * (CB + 1) * 8;
-    if (!configured) {
+    const int rc0 = once_per_device(configured, [&]() -> int {
       HP_CHECK_CUDA(cudaFuncSetAttribute(potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem));
-      configured = true;
-    }
+      return (int)HP_OK;
+    });
+    if (rc0 != HP_OK) return rc0;
     potrf_diag<<<1, 256, pd_smem, st>>>(A, lda, o, (int)n, Linv, ldi, info);
     HP_CHECK_LAUNCH("potrf_diag");
     return HP_OK;

@@ -458,11 +458,12 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
   const int64_t per = ceil_div(m, grid);
   const size_t rows_smem = (size_t)per * (PB + 1) * 8;  // panel rows + running diagonal
   const bool srows = rows_smem <= 200 * 1024;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};
+  const int rc0 = once_per_device(configured, []() -> int {
     HP_CHECK_CUDA(cudaFuncSetAttribute(pstrf_panel_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
+    return (int)HP_OK;
+  });
+  if (rc0 != HP_OK) return rc0;
   HP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &per_sm, srows ? (const void*)pstrf_panel_sm : (const void*)pstrf_panel, PT, srows ? rows_smem : 0));
   HP_REQUIRE(per_sm >= 1, "pstrf: the panel kernel does not fit on an SM");

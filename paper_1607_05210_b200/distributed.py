@@ -16,9 +16,13 @@ stays on the rank of its bottom leaf).  Because every node's arithmetic is
 the single-GPU kernel sequence with shape-only split-K plans, results are
 bitwise identical for any rank count.  With ``root_rows`` the root is instead
 evaluated by every rank on a row block of its input (rowroot.py: row
-all-to-all, all_reduced Gram, eigensolve on rank 0 + broadcast) -- needed when
-the root's input exceeds one GPU (config 3) -- and is deterministic for a
-given rank count.
+all-to-all, per-shard Grams summed in a fixed tree over 8 row shards,
+eigensolve on rank 0 + broadcast) -- needed when the root's input exceeds one
+GPU (config 3) -- and is bitwise identical for 1, 2, 4 or 8 ranks.
+
+Edges carry the child's node id in their header and the receiver checks it:
+send/recv pairs are matched by posting order only, so a placement that broke
+the order would otherwise silently hand a parent the wrong child.
 
 The driver is written against a small evaluator interface so the protocol is
 exercised on CPU (gloo, world size 2) by the tests with the CPU oracle as the
@@ -69,7 +73,8 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
 
     ``evaluator`` provides the node arithmetic and the edge payloads:
     evaluate_leaf(node), evaluate_interior(node, child_results),
-    send(result, dst, group) -> (async works, bytes), recv(src, group) -> (result, bytes);
+    send(result, dst, group, node) -> (async works, bytes), recv(src, group, node) -> (result,
+    bytes) (``node``: the child's id, carried in the payload header and verified on receipt);
     with ``root_rows`` also root_parts(result) and evaluate_root_rows(root, children, local,
     rank, world, group): the root is then evaluated by ALL ranks on row blocks of its input
     (rowroot.py) instead of gathering the children's modes on one rank."""
@@ -96,7 +101,7 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
                     child_results.append(live.pop(c))
                 else:
                     t0 = time.perf_counter()
-                    res, nbytes = evaluator.recv(place[c], group)
+                    res, nbytes = evaluator.recv(place[c], group, c)
                     stats.comm_time += time.perf_counter() - t0
                     stats.recv_bytes += nbytes
                     stats.recvs += 1
@@ -106,7 +111,7 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
         parent = maps.parent[v]
         if parent >= 0 and place[parent] != rank and v not in root_kids:
             t0 = time.perf_counter()
-            works, nbytes = evaluator.send(out, place[parent], group)
+            works, nbytes = evaluator.send(out, place[parent], group, v)
             pending_sends.extend(works)
             stats.comm_time += time.perf_counter() - t0
             stats.sent_bytes += nbytes
@@ -129,9 +134,9 @@ def run_distributed(tree: RootedTree, evaluator, rank: int, world_size: int, pla
 class DeviceEvaluator:
     """B200 node arithmetic (the same kernels as run_hapod) + NCCL payloads.
 
-    Payload of an edge: header int64 [count, d, ld, orthonormal] then sigma
-    (count float64) then the mode block storage (count x ld float64,
-    column-major) -- sent with torch.distributed isend on the NCCL backend."""
+    Payload of an edge: header int64 [node, count, d, ld, orthonormal], then sigma
+    (count float64) and the mode block storage (count x ld float64, column-major)
+    as one grouped NCCL send/recv (batch_isend_irecv)."""
 
     def __init__(self, space, leaf_blocks: dict, tol, backend=None):
         from .pod import PodBackend
@@ -170,9 +175,10 @@ class DeviceEvaluator:
         D.Profiler.set_tag(root)
         d = self.space.dimension
         layout = RR.gather_layout(children, local, rank, world, group)
-        bounds = RR.row_bounds(d, world)
+        shards = RR.row_bounds(d)
+        bounds = RR.rank_bounds(shards, world)
         S_q = RR.exchange_rows(layout, local, bounds, rank, world, arith, group)
-        res = RR.row_root_pod(S_q, layout, bounds, self.tol.epsilons[root], self.backend.gram_eig_cutoff_factor,
+        res = RR.row_root_pod(S_q, layout, shards, self.tol.epsilons[root], self.backend.gram_eig_cutoff_factor,
                               rank, world, arith, group)
         del S_q
         full = RR.gather_rows(res, d, rank, world, arith, group)
@@ -186,36 +192,41 @@ class DeviceEvaluator:
                                             "reorthonormalized": res.reorthed, "input_count": res.m,
                                             "row_blocks": res.bounds})
 
-    def send(self, ms, dst, group):
+    def send(self, ms, dst, group, node):
+        """Header [node, count, d, ld, orthonormal] (one op), then sigma and the column-major
+        mode storage as ONE grouped NCCL launch (batch_isend_irecv)."""
         import torch
         import torch.distributed as dist
         U = ms.modes_device()
-        hdr = torch.tensor([ms.count, U.rows, U.ld, int(ms.orthonormal)], dtype=torch.int64, device="cuda")
+        hdr = torch.tensor([node, ms.count, U.rows, U.ld, int(ms.orthonormal)], dtype=torch.int64, device="cuda")
         works = [dist.isend(hdr, dst, group=group)]
-        nbytes = 32
+        nbytes = 40
         if ms.count:
             sig = ms.sigmas_device().contiguous()
             body = U.storage[U.offset: U.offset + U.ld * U.cols]
-            works.append(dist.isend(sig, dst, group=group))
-            works.append(dist.isend(body, dst, group=group))
+            works.extend(dist.batch_isend_irecv([dist.P2POp(dist.isend, sig, dst, group=group),
+                                                 dist.P2POp(dist.isend, body, dst, group=group)]))
             nbytes += sig.numel() * 8 + body.numel() * 8
         return works, nbytes
 
-    def recv(self, src, group):
+    def recv(self, src, group, node):
         import torch
         import torch.distributed as dist
         from . import _device as D
         from .pod import ModeSet
-        hdr = torch.empty(4, dtype=torch.int64, device="cuda")
+        hdr = torch.empty(5, dtype=torch.int64, device="cuda")
         dist.recv(hdr, src, group=group)
-        count, d, ld, orth = (int(x) for x in hdr.tolist())
+        got, count, d, ld, orth = (int(x) for x in D.host_read(hdr))
+        if got != node:
+            raise RuntimeError(f"edge from rank {src}: expected the modes of node {node}, received node {got}")
         if count == 0:
-            return ModeSet._device(self.space, np.zeros(0), [D.Part(D.DevMat.empty(d, 0))], orthonormal=True), 32
+            return ModeSet._device(self.space, np.zeros(0), [D.Part(D.DevMat.empty(d, 0))], orthonormal=True), 40
         sig = torch.empty(count, dtype=torch.float64, device="cuda")
-        dist.recv(sig, src, group=group)
         store = torch.empty(ld * count, dtype=torch.float64, device="cuda")
-        dist.recv(store, src, group=group)
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.irecv, sig, src, group=group),
+                                         dist.P2POp(dist.irecv, store, src, group=group)]):
+            w.wait()
         U = D.DevMat(store, d, count, ld)
-        sig_host = sig.cpu().numpy()
+        sig_host = D.host_read(sig)
         ms = ModeSet._device(self.space, sig_host, [D.Part(U)], orthonormal=bool(orth), sig_dev=sig)
-        return ms, 32 + 8 * count + 8 * ld * count
+        return ms, 40 + 8 * count + 8 * ld * count

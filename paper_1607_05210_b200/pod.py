@@ -56,13 +56,14 @@ def _is_tensor(x):
 class InnerProductSpace:
     """R^d with an optional strictly positive diagonal weight vector (pod.py:43-97)."""
 
-    __slots__ = ("dimension", "weights", "_sqrt_w", "_sqrt_w_dev")
+    __slots__ = ("dimension", "weights", "_sqrt_w", "_sqrt_w_dev", "_w_dev")
 
     def __init__(self, dimension, weights=None):
         if int(dimension) != dimension or dimension < 1:
             raise ValueError(f"space dimension must be a positive integer, got {dimension}")
         object.__setattr__(self, "dimension", int(dimension))
         object.__setattr__(self, "_sqrt_w_dev", None)
+        object.__setattr__(self, "_w_dev", None)
         if weights is not None:
             w = np.asarray(weights, dtype=np.float64)
             if w.shape != (self.dimension,):
@@ -97,8 +98,26 @@ class InnerProductSpace:
             object.__setattr__(self, "_sqrt_w_dev", D.torch.from_numpy(np.array(self._sqrt_w)).to("cuda"))
         return self._sqrt_w_dev
 
-    # host-side helpers with the reference semantics (pod.py:76-97); used on
-    # small host arrays only -- the hot path never calls them
+    def weights_device(self):
+        """w as a CUDA tensor (None for the Euclidean space)."""
+        if self.weights is None:
+            return None
+        if self._w_dev is None:
+            D.require_cuda()
+            object.__setattr__(self, "_w_dev", D.torch.from_numpy(np.array(self.weights)).to("cuda"))
+        return self._w_dev
+
+    def gram(self, a, b):
+        """All pairwise inner products between the columns of ``a`` and ``b`` (pod.py:87-91):
+        ``a.T @ (w * b)``, computed by the DMMA GEMM engine.  NumPy operands give a NumPy
+        array, CUDA tensors a CUDA tensor."""
+        return D.space_gram(a, b, self.weights_device())
+
+    def norms_sq(self, a):
+        """Squared norm of every column (pod.py:93-97), computed on the device."""
+        return D.space_norms_sq(a, self.weights_device())
+
+    # host-side coordinate maps with the reference semantics (pod.py:76-84)
     def weigh(self, a):
         if self.weights is None:
             return a

@@ -10,11 +10,16 @@ evaluated with its input split by ROWS instead of gathered on rank 0:
   2. exchange  grouped point-to-point (NCCL send/recv): rank p sends rows [b_q, b_{q+1}) of
                every child block it owns to rank q, which lands them in its row block S_q
                (rows_q x m, column-major) -- an all-to-all of the sigma-scaled mode blocks.
-  3. Gram      G = sum_q S_q^T D S_q D: each rank's partial SYRK, all_reduce (sum).
+  3. Gram      G = sum_s S_s^T D S_s D over EIGHT FIXED ROW SHARDS s (independent of the
+               rank count): one SYRK per shard, the eight partials added in one fixed
+               binary tree ((0+1)+(2+3))+((4+5)+(6+7)); a sum whose operands live on two
+               ranks moves the right operand to the left one (send/recv), so every
+               rounding is the same at 1, 2, 4 or 8 ranks.
   4. eigen     rank 0 runs the node eigensolve + truncation (pod.py:329-331, 278-289) and
                broadcasts (lambda_max, nkeep, N, tail), sigma and the N kept eigenvectors.
-  5. modes     U_q = S_q D V / sigma on every rank (pod.py:333-334).
-  6. drift     C = sum_q U_q^T U_q (all_reduce), drift = max|C - I| (pod.py:245-247); above
+  5. modes     U_s = S_s D V / sigma per shard (pod.py:333-334).
+  6. drift     C = sum_s U_s^T U_s (the same fixed tree, then broadcast), drift = max|C - I|
+               (pod.py:245-247); above
                1e-8 one CholQR pass U_q <- U_q L^-T with L L^T = C computed identically on
                every rank (a second pass when the drift exceeds 1e-1) -- the span of the MGS
                sweep of pod.py:227-237.
@@ -23,8 +28,10 @@ evaluated with its input split by ROWS instead of gathered on rank 0:
 
 The protocol is written against torch.distributed and an "arith" object that provides the
 node arithmetic on one row block: ``DeviceRowArith`` (the sm_100a kernels of
-libhapod_b200.so, NCCL) here, a NumPy restatement in the CPU tests (gloo).  Results are
-deterministic for a given world size; they differ from the single-GPU root only by the
+libhapod_b200.so, NCCL) here, a NumPy restatement in the CPU tests (gloo).  Every GEMM
+runs on one fixed shard (its split-K plan depends only on the shard's shape) and every sum
+over shards follows the fixed tree, so the root's modes are bitwise identical for any rank
+count dividing the shard set; they differ from the single-GPU run_hapod root only by the
 summation order of the Gram over rows (rounding level).
 """
 
@@ -39,15 +46,64 @@ DRIFT_TOL = 1e-8          # pod.py:247
 SINGLE_PASS_DRIFT = 1e-1  # one CholQR pass is orthonormal to the rounding level below this drift
 
 
-def row_bounds(d: int, world: int, align: int = 16) -> list:
-    """Row block boundaries b_0 = 0 < ... < b_world = d, interior boundaries multiples of
+NSHARDS = 8  # fixed row shards of a distributed root: the reduction order never depends on N
+
+
+def row_bounds(d: int, nshards: int = NSHARDS, align: int = 16) -> list:
+    """Shard boundaries b_0 = 0 < ... < b_nshards = d, interior boundaries multiples of
     ``align`` (16-byte aligned column slices for the TMA GEMM)."""
     out = [0]
-    for q in range(1, world):
-        b = (d * q // world) // align * align
+    for q in range(1, nshards):
+        b = (d * q // nshards) // align * align
         out.append(max(out[-1], min(b, d)))
     out.append(d)
     return out
+
+
+def shard_owner(world: int, nshards: int = NSHARDS) -> list:
+    """shard -> rank: contiguous chunks (rank q owns shards [q n / w, (q+1) n / w))."""
+    if not 1 <= world <= nshards:
+        raise ValueError(f"the row-distributed root needs 1..{nshards} ranks, got {world}")
+    return [(s * world) // nshards for s in range(nshards)]
+
+
+def rank_bounds(shards: list, world: int) -> list:
+    """Row block of every rank: the union of its shards (contiguous)."""
+    own = shard_owner(world, len(shards) - 1)
+    out = [0] * (world + 1)
+    for q in range(world):
+        mine = [s for s in range(len(own)) if own[s] == q]
+        out[q] = shards[mine[0]] if mine else shards[-1]
+    out[world] = shards[-1]
+    for q in range(world - 1, -1, -1):  # ranks without shards: empty block at the next start
+        out[q] = min(out[q], out[q + 1])
+    return out
+
+
+def tree_reduce(partial, owner: list, rank: int, arith, group=None, lo: int = 0, hi: int | None = None):
+    """Sum of the per-shard partials over shards [lo, hi) in the FIXED binary tree
+    (left + right at every level), held by the owner of shard lo; None on other ranks.
+    ``partial(s)`` computes shard s's term (called on its owner only).  A level whose
+    operands sit on two ranks sends the right operand to the left owner (NCCL / gloo p2p);
+    at most log2(NSHARDS) + 1 partials are alive on a rank."""
+    import torch.distributed as dist
+    hi = len(owner) if hi is None else hi
+    if hi - lo == 1:
+        return partial(lo) if owner[lo] == rank else None
+    mid = (lo + hi) // 2
+    left = tree_reduce(partial, owner, rank, arith, group, lo, mid)
+    right = tree_reduce(partial, owner, rank, arith, group, mid, hi)
+    a, b = owner[lo], owner[mid]
+    if a == b:
+        return arith.add(left, right) if rank == a else None
+    if rank == b:
+        dist.send(arith.flat(right), a, group=group)
+        return None
+    if rank == a:
+        buf = arith.like(left)
+        dist.recv(arith.flat(buf), b, group=group)
+        return arith.add(left, buf)
+    return None
 
 
 @dataclass
@@ -137,16 +193,24 @@ class RowRootResult:
     m: int
 
 
-def row_root_pod(S_q, layout: RootLayout, bounds: list, eps: float, cutoff: float, rank: int, world: int, arith,
+def row_root_pod(S_q, layout: RootLayout, shards: list, eps: float, cutoff: float, rank: int, world: int, arith,
                  group=None) -> RowRootResult:
+    """Steps 3-7 on this rank's row block S_q (rows bounds[rank]..bounds[rank+1] of the root
+    input); ``shards``: the fixed shard boundaries (row_bounds)."""
     import torch
     import torch.distributed as dist
     m = layout.m
+    owner = shard_owner(world, len(shards) - 1)
+    bounds = rank_bounds(shards, world)
     r0, r1 = bounds[rank], bounds[rank + 1]
+    mine = [s for s in range(len(owner)) if owner[s] == rank]
+
+    def local(s):  # shard s as local row range of this rank's block
+        return shards[s] - r0, shards[s + 1] - r0
+
     scale = arith.vector(layout.scale)
-    # 3. Gram
-    G = arith.gram(S_q, scale)
-    dist.all_reduce(arith.flat(G), group=group)
+    # 3. Gram: per-shard SYRK, fixed-tree sum on rank 0
+    G = tree_reduce(lambda s: arith.gram_rows(S_q, *local(s), scale, m), owner, rank, arith, group)
     # 4. eigen on rank 0, broadcast
     info = arith.vector(np.zeros(4))
     if rank == 0:
@@ -164,20 +228,35 @@ def row_root_pod(S_q, layout: RootLayout, bounds: list, eps: float, cutoff: floa
         sig = arith.vector(np.zeros(n_modes))
     dist.broadcast(arith.flat(V), 0, group=group)
     dist.broadcast(sig, 0, group=group)
-    # 5. modes of this row block
-    U = arith.assemble(S_q, scale, V, sig)
+    # 5. modes of this row block, shard by shard
+    U = arith.empty_rowblock(r1 - r0, n_modes)
+    Vs = arith.scale_rows(V, scale)
     del V
-    # 6. drift and CholQR on the global Gram of the modes
-    C = arith.syrk(U)
-    dist.all_reduce(arith.flat(C), group=group)
+    for s in mine:
+        arith.assemble_rows(S_q, *local(s), Vs, sig, U)
+    del Vs
+
+    # 6. drift and CholQR on the global Gram of the modes (fixed-tree sum, broadcast)
+    def mode_gram(X):
+        C = tree_reduce(lambda s: arith.syrk_rows(X, *local(s)), owner, rank, arith, group)
+        if rank != 0:
+            C = arith.empty(n_modes, n_modes)
+        dist.broadcast(arith.flat(C), 0, group=group)
+        return C
+
+    C = mode_gram(U)
     drift = arith.drift(C)
     reorthed = False
     if drift > DRIFT_TOL:
-        U = arith.cholqr_apply(U, C)
-        if drift > SINGLE_PASS_DRIFT:
-            C = arith.syrk(U)
-            dist.all_reduce(arith.flat(C), group=group)
-            U = arith.cholqr_apply(U, C)
+        passes = 2 if drift > SINGLE_PASS_DRIFT else 1
+        for k in range(passes):
+            Linv = arith.chol_inverse(C)
+            Y = arith.empty_rowblock(r1 - r0, n_modes)
+            for s in mine:
+                arith.trmm_rows(U, *local(s), Linv, Y)
+            U = Y
+            if k + 1 < passes:
+                C = mode_gram(U)
         reorthed = True
     # 7. signs: global first-index argmax of |u| per column
     vals, idx = arith.col_absmax(U, r0)
@@ -196,12 +275,12 @@ def row_root_pod(S_q, layout: RootLayout, bounds: list, eps: float, cutoff: floa
             if v > best[0] or (v == best[0] and i < best[1]):
                 best = (v, i, q)
         win_rank[j] = best[2]
-    mine = np.where(win_rank == rank)[0]
+    mine_cols = np.where(win_rank == rank)[0]
     local_sign = np.zeros(n_modes)
-    if mine.size:
-        local_sign[mine] = arith.entry_signs(U, hi[rank, mine] - r0, mine)
+    if mine_cols.size:
+        local_sign[mine_cols] = arith.entry_signs(U, hi[rank, mine_cols] - r0, mine_cols)
     sgn = arith.vector(local_sign)
-    dist.all_reduce(sgn, group=group)
+    dist.all_reduce(sgn, group=group)  # exactly one nonzero (+-1) term per column
     s = arith.to_host(sgn)
     s = np.where(s < 0.0, -1.0, 1.0)
     U = arith.flip(U, arith.vector(s))
@@ -300,9 +379,24 @@ class DeviceRowArith:
     def copy_rows_into(self, block, full, r0):
         self._copy(block, 0, block.rows, full, r0, 0)
 
+    def like(self, M):
+        return self.D.DevMat(self.torch.empty_like(M.storage), M.rows, M.cols, M.ld, M.offset)
+
+    def rows_view(self, M, a, b):
+        return self.D.DevMat(M.storage, b - a, M.cols, M.ld, M.offset + a)
+
     # -- arithmetic
-    def gram(self, S, scale):
-        G, _, _ = self.D.gram_full([self.D.Part(S, scale)], S.rows)
+    def add(self, A, B):
+        """A <- A + B elementwise (the fixed-tree shard sum)."""
+        n = A.ld * A.cols
+        if n:
+            self.N.check(self.lib.hp_add(A.ptr, B.ptr, n, self.D._stream()), "partial sum")
+        return A
+
+    def gram_rows(self, S, a, b, scale, m):
+        if b <= a:
+            return self.D.DevMat.empty(m, m, zero=True)
+        G, _, _ = self.D.gram_full([self.D.Part(self.rows_view(S, a, b), scale)], b - a)
         return G
 
     def eig(self, G, m, eps, cutoff):
@@ -313,39 +407,45 @@ class DeviceRowArith:
         self._copy(ev.Vn, 0, m, V, 0, 0)
         return ev.lam_max, ev.nkeep, ev.n_modes, ev.tail, V, ev.sig_dev.contiguous()
 
-    def assemble(self, S, scale, V, sig):
+    def scale_rows(self, V, scale):
         m, n = V.rows, V.cols
         Vs = self.empty(m, n)
-        st = self.D._stream()
-        self.N.check(self.lib.hp_scale(V.ptr, V.ld, m, n, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st), "scale V")
-        U = self.empty(S.rows, n)
-        if S.rows:
-            ws = self.D._ws(self.lib.hp_assemble_workspace_bytes(S.rows, m, n))
-            with self.D._phase("assemble", 2.0 * S.rows * m * n):
-                self.N.check(self.lib.hp_assemble(S.vecset(), S.rows, m, Vs.ptr, Vs.ld, sig.data_ptr(), n, U.ptr, U.ld,
-                                                  ws.data_ptr(), ws.numel(), st), "assemble")
-        return U
+        self.N.check(self.lib.hp_scale(V.ptr, V.ld, m, n, scale.data_ptr(), None, None, Vs.ptr, Vs.ld,
+                                       self.D._stream()), "scale V")
+        return Vs
 
-    def syrk(self, U):
+    def assemble_rows(self, S, a, b, Vs, sig, U):
+        """rows [a, b) of U <- rows [a, b) of S times Vs / sigma (pod.py:333-334)."""
+        if b <= a:
+            return
+        m, n = Vs.rows, Vs.cols
+        Sv, Uv = self.rows_view(S, a, b), self.rows_view(U, a, b)
+        ws = self.D._ws(self.lib.hp_assemble_workspace_bytes(b - a, m, n))
+        with self.D._phase("assemble", 2.0 * (b - a) * m * n):
+            self.N.check(self.lib.hp_assemble(Sv.vecset(), b - a, m, Vs.ptr, Vs.ld, sig.data_ptr(), n, Uv.ptr, Uv.ld,
+                                              ws.data_ptr(), ws.numel(), self.D._stream()), "assemble")
+
+    def syrk_rows(self, U, a, b):
         n = U.cols
+        if b <= a:
+            return self.D.DevMat.empty(n, n, zero=True)
         C = self.empty(n, n)
-        if U.rows:
-            ws = self.D._ws(self.lib.hp_gram_workspace_bytes(U.rows, n))
-            with self.D._phase("drift", float(U.rows) * n * (n + 1)):
-                self.N.check(self.lib.hp_gram(U.vecset(), U.rows, n, None, C.ptr, C.ld, ws.data_ptr(), ws.numel(),
-                                              self.D._stream()), "U^T U")
-        else:
-            C.storage.zero_()
+        Uv = self.rows_view(U, a, b)
+        ws = self.D._ws(self.lib.hp_gram_workspace_bytes(b - a, n))
+        with self.D._phase("drift", float(b - a) * n * (n + 1)):
+            self.N.check(self.lib.hp_gram(Uv.vecset(), b - a, n, None, C.ptr, C.ld, ws.data_ptr(), ws.numel(),
+                                          self.D._stream()), "U^T U")
         return C
 
     def drift(self, C):
         out = self.torch.zeros(1, dtype=self.torch.float64, device="cuda")
         self.N.check(self.lib.hp_gram_drift(C.ptr, C.ld, C.rows, out.data_ptr(), self.D._stream()), "drift")
-        return float(out.item())
+        return float(self.D.host_read(out)[0])
 
-    def cholqr_apply(self, U, C):
-        n = U.cols
-        Cw = self.D.DevMat(C.storage.clone(), n, n, C.ld)
+    def chol_inverse(self, C):
+        """L^{-1} for C = L L^T (identical on every rank: same input, same kernels)."""
+        n = C.cols
+        Cw = self.D.DevMat(C.storage.clone(), n, n, C.ld, C.offset)
         Linv = self.empty(n, n)
         ws = self.D._ws(self.lib.hp_chol_inverse_workspace_bytes(n))
         info = ctypes.c_int(0)
@@ -353,14 +453,19 @@ class DeviceRowArith:
                                               ws.numel(), self.D._stream()), "CholQR factor")
         if info.value != 0:
             raise np.linalg.LinAlgError("row-distributed CholQR: the modes' Gram is not positive definite")
-        Y = self.empty(U.rows, n)
-        if U.rows:
-            gws = self.D._ws(self.lib.hp_gemm_workspace_bytes(U.rows, n, n, 0, 1))
-            with self.D._phase("reortho", float(U.rows) * n * n):
-                self.N.check(self.lib.hp_gemm(0, 0, U.rows, n, n, U.vecset(), Linv.vecset(), 1.0, 0.0, Y.ptr, Y.ld,
-                                              None, None, None, 0, 1, gws.data_ptr(), gws.numel(), self.D._stream()),
-                             "U L^-T")
-        return Y
+        return Linv
+
+    def trmm_rows(self, U, a, b, Linv, Y):
+        """rows [a, b) of Y <- rows [a, b) of U times L^{-T} (upper triangular operand)."""
+        if b <= a:
+            return
+        n = U.cols
+        Uv, Yv = self.rows_view(U, a, b), self.rows_view(Y, a, b)
+        gws = self.D._ws(self.lib.hp_gemm_workspace_bytes(b - a, n, n, 0, 1))
+        with self.D._phase("reortho", float(b - a) * n * n):
+            self.N.check(self.lib.hp_gemm(0, 0, b - a, n, n, Uv.vecset(), Linv.vecset(), 1.0, 0.0, Yv.ptr, Yv.ld,
+                                          None, None, None, 0, 1, gws.data_ptr(), gws.numel(), self.D._stream()),
+                         "U L^-T")
 
     def col_absmax(self, U, row_offset):
         n = U.cols

@@ -32,25 +32,26 @@ class OracleEvaluator:
         stacked = np.hstack(parts) if parts else np.zeros((d, 0))
         return O.pod(stacked, self.eps[node])
 
-    def send(self, res, dst, group):
-        hdr = torch.tensor([res.count, res.modes.shape[0], int(res.orthonormal)], dtype=torch.int64)
+    def send(self, res, dst, group, node):
+        hdr = torch.tensor([node, res.count, res.modes.shape[0], int(res.orthonormal)], dtype=torch.int64)
         works = [dist.isend(hdr, dst, group=group)]
         if res.count:
             works.append(dist.isend(torch.from_numpy(np.ascontiguousarray(res.sigmas)), dst, group=group))
             works.append(dist.isend(torch.from_numpy(np.ascontiguousarray(res.modes.T)), dst, group=group))
-        return works, 24 + 8 * res.count * (1 + res.modes.shape[0])
+        return works, 32 + 8 * res.count * (1 + res.modes.shape[0])
 
-    def recv(self, src, group):
-        hdr = torch.empty(3, dtype=torch.int64)
+    def recv(self, src, group, node):
+        hdr = torch.empty(4, dtype=torch.int64)
         dist.recv(hdr, src, group=group)
-        n, d, orth = (int(x) for x in hdr.tolist())
+        got, n, d, orth = (int(x) for x in hdr.tolist())
+        assert got == node, (got, node)
         if n == 0:
-            return O.Modes(np.zeros(0), np.zeros((d, 0))), 24
+            return O.Modes(np.zeros(0), np.zeros((d, 0))), 32
         sig = torch.empty(n, dtype=torch.float64)
         dist.recv(sig, src, group=group)
         modes = torch.empty((n, d), dtype=torch.float64)
         dist.recv(modes, src, group=group)
-        return O.Modes(sig.numpy().copy(), modes.numpy().T.copy(), bool(orth)), 24 + 8 * n * (1 + d)
+        return O.Modes(sig.numpy().copy(), modes.numpy().T.copy(), bool(orth)), 32 + 8 * n * (1 + d)
 
 
 def _case(kind):
@@ -160,9 +161,16 @@ class NumpyRowArith:
     def _np(M):
         return M.numpy().T
 
-    def gram(self, S, scale):
-        a = self._np(S) * scale.numpy()[None, :]
-        g = a.T @ a
+    def like(self, M):
+        return torch.empty_like(M)
+
+    def add(self, A, B):
+        A += B
+        return A
+
+    def gram_rows(self, S, a, b, scale, m):
+        x = self._np(S)[a:b] * scale.numpy()[None, :]
+        g = x.T @ x
         return torch.from_numpy(np.ascontiguousarray(0.5 * (g + g.T)))
 
     def eig(self, G, m, eps, cutoff):
@@ -180,23 +188,29 @@ class NumpyRowArith:
         V = torch.from_numpy(np.ascontiguousarray(psi[:, keep][:, :n].T))
         return lam_max, int(keep.sum()), n, tail, V, torch.from_numpy(sig[:n].copy())
 
-    def assemble(self, S, scale, V, sig):
-        u = (self._np(S) * scale.numpy()[None, :]) @ self._np(V) / sig.numpy()[None, :]
-        return torch.from_numpy(np.ascontiguousarray(u.T))
+    def scale_rows(self, V, scale):
+        return V * scale[None, :]
 
-    def syrk(self, U):
-        u = self._np(U)
+    def assemble_rows(self, S, a, b, Vs, sig, U):
+        u = self._np(S)[a:b] @ self._np(Vs) / sig.numpy()[None, :]
+        U[:, a:b] = torch.from_numpy(np.ascontiguousarray(u.T))
+
+    def syrk_rows(self, U, a, b):
+        u = self._np(U)[a:b]
         return torch.from_numpy(np.ascontiguousarray(u.T @ u))
 
     def drift(self, C):
         c = C.numpy()
         return float(np.abs(c - np.eye(c.shape[0])).max()) if c.size else 0.0
 
-    def cholqr_apply(self, U, C):
+    def chol_inverse(self, C):
         import scipy.linalg
         L = np.linalg.cholesky(C.numpy())
-        y = scipy.linalg.solve_triangular(L, self._np(U).T, lower=True).T  # U L^{-T}
-        return torch.from_numpy(np.ascontiguousarray(y.T))
+        return torch.from_numpy(scipy.linalg.solve_triangular(L, np.eye(L.shape[0]), lower=True))
+
+    def trmm_rows(self, U, a, b, Linv, Y):
+        y = self._np(U)[a:b] @ Linv.numpy().T  # U L^{-T}
+        Y[:, a:b] = torch.from_numpy(np.ascontiguousarray(y.T))
 
     def col_absmax(self, U, row_offset):
         u = np.abs(self._np(U))
@@ -226,9 +240,10 @@ class RowOracleEvaluator(OracleEvaluator):
         from paper_1607_05210_b200 import rowroot as RR
         arith = NumpyRowArith()
         layout = RR.gather_layout(children, local, rank, world, group)
-        bounds = RR.row_bounds(self.d, world, align=2)
+        shards = RR.row_bounds(self.d, align=2)
+        bounds = RR.rank_bounds(shards, world)
         S = RR.exchange_rows(layout, local, bounds, rank, world, arith, group)
-        res = RR.row_root_pod(S, layout, bounds, self.eps[root], O.DEFAULT_GRAM_CUTOFF, rank, world, arith, group)
+        res = RR.row_root_pod(S, layout, shards, self.eps[root], O.DEFAULT_GRAM_CUTOFF, rank, world, arith, group)
         full = RR.gather_rows(res, self.d, rank, world, arith, group)
         if rank != 0:
             return None
@@ -247,6 +262,49 @@ def _row_worker(rank, world, port, kind, out_q):
         out_q.put((rank, None if root is None else (root.sigmas, root.modes, root.tail_energy)))
     finally:
         dist.destroy_process_group()
+
+
+def _row_run(kind, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    msgs = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(msgs[r] is None for r in range(1, world))
+    return msgs[0]
+
+
+def test_row_distributed_root_bitwise_across_rank_counts():
+    """the root's Gram and mode Gram are summed over 8 FIXED row shards in one
+    fixed binary tree, and every product runs on one shard -- so 1, 2, 4 and 8 ranks produce
+    bitwise identical sigma, modes and tail (the reference is bit-identical across worker
+    counts, tests/test_parallel.py:50-58)."""
+    runs = {w: _row_run("star", w) for w in (1, 2, 4, 8)}
+    s1, m1, t1 = runs[1]
+    for w in (2, 4, 8):
+        s, mo, t = runs[w]
+        assert np.array_equal(s, s1), w
+        assert np.array_equal(mo, m1), w
+        assert t == t1, w
+
+
+def test_row_bounds_and_owners():
+    from paper_1607_05210_b200 import rowroot as RR
+    sh = RR.row_bounds(200_000)
+    assert len(sh) == 9 and sh[0] == 0 and sh[-1] == 200_000
+    assert all(b % 16 == 0 for b in sh[1:-1]) and all(x <= y for x, y in zip(sh, sh[1:]))
+    for w in (1, 2, 3, 4, 5, 8):
+        own = RR.shard_owner(w)
+        assert own[0] == 0 and own[-1] == w - 1 and own == sorted(own)
+        rb = RR.rank_bounds(sh, w)
+        assert rb[0] == 0 and rb[-1] == 200_000 and rb == sorted(rb)
+    with pytest.raises(ValueError):
+        RR.shard_owner(9)
 
 
 @pytest.mark.parametrize("kind,world", [("star", 2), ("star", 3), ("balanced", 3)])

@@ -171,24 +171,42 @@ def test_syev_graded_psd_gram():
     assert np.max(np.abs(v.T @ v - np.eye(m))) < 1e-13
 
 
-def test_truncate_kernel_matches_rule():
+def _ref_truncate(lam, eps, cutoff, m):
+    """pod.py:281-289 verbatim arithmetic: keep mask, sqrt, truncation_rank, np.sum tail."""
     from oracle.hapod_oracle import truncation_rank
-    rng = np.random.default_rng(9)
-    for trial in range(20):
-        n = int(rng.integers(1, 3000))
-        lam = np.sort(rng.exponential(1.0, n) ** 4)[::-1]
-        eps = float(rng.uniform(0, 1) * np.sqrt(lam.sum()))
-        cutoff = 4 * 2.0 ** -52
-        ld = torch.from_numpy(lam.copy()).cuda()
-        sig = torch.empty(n, dtype=torch.float64, device="cuda")
-        info = torch.empty(4, dtype=torch.float64, device="cuda")
-        N.check(lib.hp_truncate(ld.data_ptr(), n, eps, cutoff, n, sig.data_ptr(), info.data_ptr(), st()), "trunc")
-        lam_max, nkeep, N_, tail = info.cpu().tolist()
-        keep = lam >= cutoff * lam[0] * n
-        s = np.sqrt(lam[keep])
-        assert int(nkeep) == keep.sum()
-        assert int(N_) == truncation_rank(s, eps)
-        assert tail == pytest.approx(float(np.sum(lam[keep][int(N_):])), rel=1e-12, abs=1e-300)
+    keep = lam >= cutoff * lam[0] * m
+    lk = lam[keep]
+    s = np.sqrt(lk)
+    n = truncation_rank(s, eps)
+    return int(keep.sum()), n, float(np.sum(lk[n:])), s
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_truncate_kernel_bitwise(seed):
+    """K3 bit-for-bit against the reference's NumPy arithmetic: the count, N, every sigma and
+    the tail energy (sequential reversed cumsum of sigma*sigma, pairwise np.sum) -- including
+    budgets placed exactly on a tail value and one ulp either side of it."""
+    rng = np.random.default_rng(900 + seed)
+    cutoff = 4 * 2.0 ** -52
+    for trial in range(30):
+        n = int(rng.integers(1, 20000 if trial % 5 == 0 else 3000))
+        lam = np.sort(rng.exponential(1.0, n) ** 4 * 10.0 ** rng.uniform(-12, 0, n))[::-1].copy()
+        s = np.sqrt(lam[lam >= cutoff * lam[0] * n])
+        tails = np.cumsum((s * s)[::-1])[::-1]
+        k = int(rng.integers(0, s.size))
+        base = float(np.sqrt(tails[k]))
+        for eps in (float(rng.uniform(0, 1) * np.sqrt(lam.sum())), base, np.nextafter(base, 0.0),
+                    np.nextafter(base, np.inf), 0.0):
+            ld = torch.from_numpy(lam.copy()).cuda()
+            sig = torch.empty(n, dtype=torch.float64, device="cuda")
+            info = torch.empty(4, dtype=torch.float64, device="cuda")
+            N.check(lib.hp_truncate(ld.data_ptr(), n, eps, cutoff, n, sig.data_ptr(), info.data_ptr(), st()),
+                    "trunc")
+            lam_max, nkeep, N_, tail = info.cpu().tolist()
+            rk, rn, rtail, rs = _ref_truncate(lam, eps, cutoff, n)
+            assert int(nkeep) == rk and int(N_) == rn, (trial, eps)
+            assert tail == rtail, (trial, eps, tail, rtail)
+            assert np.array_equal(sig.cpu().numpy()[:rk], rs)
 
 
 def test_signs_and_reortho():

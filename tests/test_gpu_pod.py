@@ -311,3 +311,31 @@ def test_deferred_upload_matches_eager_and_checks_finiteness():
     blk = H.SnapshotBlock(sp, bad, defer_upload=True)  # no check yet
     with pytest.raises(ValueError):
         H.pod(blk, 0.1)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("d,p,q", [(1, 1, 1), (37, 5, 9), (5000, 64, 130), (20000, 3, 1)])
+def test_space_gram_and_norms(weighted, d, p, q):
+    """InnerProductSpace.gram / .norms_sq (pod.py:87-97) on the device vs the reference
+    arithmetic (oracle ip_gram / ip_norms_sq): host operands in, NumPy out; device in, device out."""
+    rng = np.random.default_rng(d + p + q)
+    w = rng.uniform(0.5, 2.0, d) if weighted else None
+    sp = H.InnerProductSpace(d, w)
+    a = rng.standard_normal((d, p))
+    b = rng.standard_normal((d, q))
+    g = sp.gram(a, b)
+    assert isinstance(g, np.ndarray) and g.shape == (p, q)
+    ref = O.ip_gram(a, b, w)
+    assert np.allclose(g, ref, rtol=1e-13, atol=1e-13 * math.sqrt(d))
+    ns = sp.norms_sq(a)
+    assert isinstance(ns, np.ndarray) and ns.shape == (p,)
+    assert np.allclose(ns, O.ip_norms_sq(a, w), rtol=1e-13)
+    gd = sp.gram(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert gd.is_cuda and np.allclose(gd.cpu().numpy(), ref, rtol=1e-13, atol=1e-13 * math.sqrt(d))
+    assert np.allclose(sp.norms_sq(torch.from_numpy(a).cuda()).cpu().numpy(), O.ip_norms_sq(a, w), rtol=1e-13)
+
+
+def test_space_gram_rejects_mismatched_rows():
+    sp = H.InnerProductSpace(10)
+    with pytest.raises(ValueError):
+        sp.gram(np.ones((10, 2)), np.ones((11, 2)))
