@@ -36,23 +36,46 @@ def metrics(dev_sig, dev_modes, ref):
     return rel, ang
 
 
-def tree_floors(children, root, blocks, eps, ref):
+class Floors(tuple):
+    """(max rel dsigma, max angle sine, count mismatch) of the CPU-vs-CPU variants, plus
+    ``l2``: the largest relative difference of their projection errors (filled by l2_floor)."""
+    l2 = 0.0
+
+
+def l2_gate(floors):
+    """Projection l2 parity gate: 1e-8 relative (BASELINE.json), or 4x the CPU-vs-CPU floor where the
+    residual is so far below ||S||_F that the modes' permitted orthonormality drift (<= 1e-8,
+    pod.py:247) already moves it by more than that (config 3: l2 = 1e-3 eps*, the noise level)."""
+    return max(1e-8, 4.0 * floors.l2)
+
+
+def tree_floors(children, root, blocks, eps, ref, ref_err=None):
     """CPU-vs-CPU floors of a tree run: the oracle with LAPACK divide and conquer
     (evd) and the oracle (evr) on row-permuted snapshots, each against the reference-order run.
-    Returns (max rel dsigma, max angle sine, count mismatch) over both variants."""
+    Returns Floors(max rel dsigma, max angle sine, count mismatch) over both variants; with
+    ``ref_err`` (the reference-order run's total l2 error) also the l2 floor."""
     d = next(iter(blocks.values())).shape[0]
     perm = np.random.default_rng(99).permutation(d)
     pb = {k: np.asfortranarray(v[perm]) for k, v in blocks.items()}
     runs = [(O.run_hapod(children, root, blocks, eps, driver="evd").modes, None),
             (O.run_hapod(children, root, pb, eps).modes, np.argsort(perm))]
-    frel, fang, dcount = 0.0, 0.0, 0
+    frel, fang, dcount, fl2 = 0.0, 0.0, 0, 0.0
+    order = sorted(blocks)
+    vals = np.hstack([blocks[k] for k in order]) if ref_err is not None else None
     for mo, inv in runs:
         modes = mo.modes if inv is None else mo.modes[inv]
         r, a = metrics(mo.sigmas, modes, ref)
         frel = max(frel, float(r.max()) if r.size else 0.0)
         fang = max(fang, float(a.max()) if a.size else 0.0)
         dcount = max(dcount, abs(mo.count - ref.count))
-    return frel, fang, dcount
+        if ref_err is not None and ref_err > 0.0:
+            e = math.sqrt(O.actual_mean_error(vals, modes) * vals.shape[1])
+            fl2 = max(fl2, abs(e - ref_err) / ref_err)
+    out = Floors((frel, fang, dcount))
+    out.l2 = fl2
+    if ref_err is not None:
+        print(f"\n[floors] CPU-vs-CPU relative l2 difference {fl2:.3e}")
+    return out
 
 
 def report(name, dev_count, ref_count, rel, ang, frel=None, fang=None, extra=""):
@@ -61,21 +84,23 @@ def report(name, dev_count, ref_count, rel, ang, frel=None, fang=None, extra="")
           + (f"; CPU-vs-CPU floor: rel dsigma={frel:.3e}, angle={fang:.3e}" if frel is not None else "") + extra)
 
 
+
 def test_config0_full_size():
     """Config 0 at its full size (20,000 x 1,000): single POD, eps* = 1e-4 ||S||_F."""
     wl = W.make(0)
     vals = host(wl.values)
     out = H.pod(H.SnapshotBlock(H.InnerProductSpace(wl.d), wl.values), wl.eps_star)
     ref = O.pod(vals, wl.eps_star)
-    frel, fang, fcount = tree_floors([[]], 0, {0: vals}, [wl.eps_star], ref)
+    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes) * wl.m)
+    fl = tree_floors([[]], 0, {0: vals}, [wl.eps_star], ref, ref_err)
+    frel, fang, fcount = fl
     rel, ang = metrics(out.sigmas, out.modes, ref)
     err = math.sqrt(H.actual_mean_error(H.SnapshotBlock(H.InnerProductSpace(wl.d), wl.values), out) * wl.m)
-    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes) * wl.m)
     report("c0", out.count, ref.count, rel, ang, frel, fang,
            f"; l2 gpu={err:.6e} cpu={ref_err:.6e} eps*={wl.eps_star:.6e}")
     assert out.count == ref.count == 500
     assert rel.max() <= max(1e-10, 4.0 * frel)
-    assert abs(err - ref_err) <= 1e-8 * ref_err
+    assert abs(err - ref_err) <= l2_gate(fl) * ref_err
     assert err <= wl.eps_star
     assert ang.max() <= max(1e-8, 4.0 * fang)
 
@@ -96,17 +121,18 @@ def test_config1_star_reduced(d):
     order = H.derive_maps(tree).leaf_order
     blocks = {leaf: vals[:, 512 * i: 512 * (i + 1)] for i, leaf in enumerate(order)}
     ref = O.run_hapod(children, 0, blocks, list(tol.epsilons))
-    frel, fang, fcount = tree_floors(children, 0, blocks, list(tol.epsilons), ref.modes)
+    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
+    fl = tree_floors(children, 0, blocks, list(tol.epsilons), ref.modes, ref_err)
+    frel, fang, fcount = fl
     rel, ang = metrics(res.modes.sigmas, res.modes.modes, ref.modes)
     err = math.sqrt(H.actual_mean_error(blk, res.modes) * m)
-    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
     report(f"c1-mini d={d} m={m}", res.mode_count, ref.modes.count, rel, ang, frel, fang,
            f"; floor count diff {fcount}; l2 gpu={err:.6e} cpu={ref_err:.6e}")
     # no slack: identical counts, every kept sigma, the angle and the projection error
     assert res.mode_count == ref.modes.count
     assert rel.max() <= max(1e-10, 4.0 * frel)
     assert ang.max() <= max(1e-8, 4.0 * fang)
-    assert abs(err - ref_err) <= 1e-8 * ref_err
+    assert abs(err - ref_err) <= l2_gate(fl) * ref_err
 
 
 def test_config2_chain_reduced():
@@ -149,17 +175,18 @@ def test_config3_star_reduced():
     order = H.derive_maps(tree).leaf_order
     blocks = {leaf: vals[:, 512 * i: 512 * (i + 1)] for i, leaf in enumerate(order)}
     ref = O.run_hapod(children, 0, blocks, list(tol.epsilons))
-    frel, fang, fcount = tree_floors(children, 0, blocks, list(tol.epsilons), ref.modes)
+    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
+    fl = tree_floors(children, 0, blocks, list(tol.epsilons), ref.modes, ref_err)
+    frel, fang, fcount = fl
     rel, ang = metrics(res.modes.sigmas, res.modes.modes, ref.modes)
     err = math.sqrt(H.actual_mean_error(blk, res.modes) * m)
-    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
     leaf_counts = sorted({r.output_mode_count for r in res.reports if r.is_leaf})
     report("c3-mini", res.mode_count, ref.modes.count, rel, ang, frel, fang,
            extra=f"; leaf modes {leaf_counts}; l2 gpu={err:.4e} cpu={ref_err:.4e} eps*={wl.eps_star:.4e}")
     assert res.mode_count == ref.modes.count
     assert rel.max() <= max(1e-10, 4.0 * frel)
     assert ang.max() <= max(1e-8, 4.0 * fang)
-    assert abs(err - ref_err) <= 1e-8 * ref_err
+    assert abs(err - ref_err) <= l2_gate(fl) * ref_err
     assert err <= wl.eps_star
 
 
@@ -188,14 +215,15 @@ def test_config4_chains_under_root_reduced():
     blocks = {leaf: vals[:, 512 * i: 512 * (i + 1)] for i, leaf in enumerate(order)}
     ch = [list(c) for c in tree.children]
     ref = O.run_hapod(ch, 0, blocks, list(tol.epsilons))
-    frel, fang, fcount = tree_floors(ch, 0, blocks, list(tol.epsilons), ref.modes)
+    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
+    fl = tree_floors(ch, 0, blocks, list(tol.epsilons), ref.modes, ref_err)
+    frel, fang, fcount = fl
     rel, ang = metrics(res.modes.sigmas, res.modes.modes, ref.modes)
     err = math.sqrt(H.actual_mean_error(blk, res.modes) * m)
-    ref_err = math.sqrt(O.actual_mean_error(vals, ref.modes.modes) * m)
     report("c4-mini", res.mode_count, ref.modes.count, rel, ang, frel, fang,
            extra=f"; l2 gpu={err:.4e} cpu={ref_err:.4e} eps*={wl.eps_star:.4e}")
     assert res.mode_count == ref.modes.count
     assert rel.max() <= max(1e-10, 4.0 * frel)
     assert ang.max() <= max(1e-8, 4.0 * fang)
-    assert abs(err - ref_err) <= 1e-8 * ref_err
+    assert abs(err - ref_err) <= l2_gate(fl) * ref_err
     assert err <= wl.eps_star
