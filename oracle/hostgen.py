@@ -60,3 +60,44 @@ def checksum(a: np.ndarray) -> np.ndarray:
     cols = np.arange(0, a.shape[1], max(1, a.shape[1] // 61))
     rows = np.arange(0, a.shape[0], max(1, a.shape[0] // 53))
     return np.concatenate([[np.linalg.norm(a)], a[:, cols].sum(axis=0), a[np.ix_(rows, cols)].reshape(-1)])
+
+
+# ---------------------------------------------------------------------------- configs 2-4 (timing samples)
+def pulse(d: int, cols: np.ndarray, seed: int) -> np.ndarray:
+    """BASELINE config 2 columns: u_j(x) = exp(-(x - 0.1 - 0.8 t_j)^2 / (2 w_j^2)) on x = linspace(0, 1, d),
+    t_j ~ U[0,1], w_j ~ U[0.01, 0.05] per column id (the same Philox streams as the device generator)."""
+    rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 2])))
+    nmax = int(cols.max()) + 1 if cols.size else 0
+    t = rng.uniform(0.0, 1.0, nmax)[cols]
+    w = rng.uniform(0.01, 0.05, nmax)[cols]
+    x = np.linspace(0.0, 1.0, d)
+    z = (x[:, None] - 0.1 - 0.8 * t[None, :]) / w[None, :]
+    return np.asfortranarray(np.exp(-0.5 * z * z))
+
+
+def sine(d: int, cols: np.ndarray, seed: int, noise_key: int = 0, modes: int = 300, noise: float = 1e-8) -> np.ndarray:
+    """BASELINE config 3 columns: sum_{k<=300} k^-2 a_jk sin(k pi x) + 1e-8 N(0,1).  The coefficient
+    stream is the device generator's; the noise stream is NumPy's (the device draws it with the
+    CUDA generator), so these are statistically -- not bytewise -- the device's columns: they
+    serve the CPU timing samples of bench.py only."""
+    rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 3])))
+    nmax = int(cols.max()) + 1 if cols.size else 0
+    a = rng.standard_normal((max(nmax, 1), modes))[cols] / (np.arange(1, modes + 1) ** 2)[None, :]
+    x = np.linspace(0.0, 1.0, d)
+    basis = np.sin(np.pi * np.arange(1, modes + 1)[None, :] * x[:, None])  # (d, modes)
+    out = basis @ a.T
+    nrng = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 5, int(noise_key)])))
+    out += noise * nrng.standard_normal(out.shape)
+    return np.asfortranarray(out)
+
+
+def mixed(d: int, cols: np.ndarray, m_total: int, seed: int, noise_key: int = 0) -> np.ndarray:
+    """BASELINE config 4 columns: half sine field, half pulses, interleaved by a seeded permutation."""
+    perm = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 4]))).permutation(m_total)
+    is_sine = perm[cols] < m_total // 2
+    out = np.empty((d, cols.size), order="F")
+    if is_sine.any():
+        out[:, is_sine] = sine(d, cols[is_sine], seed, noise_key)
+    if (~is_sine).any():
+        out[:, ~is_sine] = pulse(d, cols[~is_sine], seed)
+    return out
