@@ -53,6 +53,7 @@ struct Params {
   double* partial;
   int tiles_m, tiles_n;
   int64_t ntiles;
+  int bn;  // tile width in n: 128, or 96 / 64 for narrow NN / TN outputs on the TMA path (K-major B)
 };
 
 template <bool AK, bool BKM>
@@ -216,19 +217,19 @@ __device__ __forceinline__ void mma_ktile(const double* as, const double* bs, do
 }
 
 // Epilogue: split-K partial tile, or alpha/beta/row-col scale/divide + symmetric mirror into C.
-template <bool AK, bool BKM>
-__device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8][4][2], int64_t tile, int z, int64_t m0,
+template <bool AK, bool BKM, int NJ = 4>
+__device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8][NJ][2], int64_t tile, int z, int64_t m0,
                                          int64_t n0, int wm, int wn, int g, int t) {
   if (p.splits > 1) {
-    double* out = p.partial + ((int64_t)z * p.ntiles + tile) * (BM * BN);
+    double* out = p.partial + ((int64_t)z * p.ntiles + tile) * (BM * (8 * NJ * 4));
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int ml = wm * 64 + (AK ? i * 8 + g : g * 8 + i);
-          const int nl = wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+          const int nl = wn * (8 * NJ) + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
           out[nl * BM + ml] = acc[i][j][e];
         }
     return;
@@ -236,11 +237,11 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t m = m0 + wm * 64 + (AK ? i * 8 + g : g * 8 + i);
-        const int64_t n = n0 + wn * 32 + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+        const int64_t n = n0 + wn * (8 * NJ) + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
         if (m >= p.M || n >= p.N) continue;
         if (p.sym && m > n) continue;
         double v = p.alpha * acc[i][j][e];
@@ -344,33 +345,34 @@ __device__ __forceinline__ int mmaj_off(int m, int k) {
   return (m >> 4) * 2048 + k * 128 + (((((m & 15) >> 1) ^ k) & 7) << 4) + (m & 1) * 8;
 }
 
-template <bool AK, bool BKM>
-__device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, double (&acc)[8][4][2], int wm, int wn,
+template <bool AK, bool BKM, int NJ>
+__device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, double (&acc)[8][NJ][2], int wm, int wn,
                                              int g, int t) {
-  if (AK && BKM) {
+  static_assert(BKM || NJ == 4, "narrow n tiles need a K-major B operand");
+  if constexpr (AK && BKM) {
 #pragma unroll
     for (int sp = 0; sp < 2; ++sp) {
-      double2 af[8], bf[4];
+      double2 af[8], bf[NJ];
       const int kk = 4 * t + 2 * sp;
 #pragma unroll
       for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double2*>(as + kmaj_off(wm * 64 + i * 8 + g, kk));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double2*>(bs + kmaj_off(wn * 32 + j * 8 + g, kk));
+      for (int j = 0; j < NJ; ++j) bf[j] = *reinterpret_cast<const double2*>(bs + kmaj_off(wn * (8 * NJ) + j * 8 + g, kk));
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j], af[i].x, bf[j].x);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j], af[i].y, bf[j].y);
     }
   } else {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      double af[8], bf[4];
+      double af[8], bf[NJ];
       const int kk = 4 * s + t;
-      if (AK) {
+      if constexpr (AK) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double*>(as + kmaj_off(wm * 64 + i * 8 + g, kk));
       } else {
@@ -381,9 +383,9 @@ __device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, dou
           af[2 * q + 1] = v.y;
         }
       }
-      if (BKM) {
+      if constexpr (BKM) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double*>(bs + kmaj_off(wn * 32 + j * 8 + g, kk));
+        for (int j = 0; j < NJ; ++j) bf[j] = *reinterpret_cast<const double*>(bs + kmaj_off(wn * (8 * NJ) + j * 8 + g, kk));
       } else {
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -395,12 +397,12 @@ __device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, dou
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
   }
 }
 
-template <bool AK, bool BKM>
+template <bool AK, bool BKM, int NJ>
 __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
   const Params& p = tp.p;
   extern __shared__ __align__(16) double smem[];
@@ -414,10 +416,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
   const int z = blockIdx.z;
   int bi, bj;
   tile_coords(p, tile, bi, bj);
-  const int64_t m0 = (int64_t)bi * BM, n0 = (int64_t)bj * BN;
+  constexpr int TBN = 32 * NJ;                 // tile width in n (4 n-warps x NJ fragments of 8)
+  constexpr int B_BYTES = TBN * BK * 8;
+  constexpr int STAGE_BYTES = TILE_BYTES + B_BYTES;
+  const int64_t m0 = (int64_t)bi * BM, n0 = (int64_t)bj * TBN;
   const int64_t kbeg = (int64_t)z * p.kspan;
   int64_t kend = min(p.K, kbeg + p.kspan);
-  if (p.b_upper) kend = min(kend, n0 + BN);
+  if (p.b_upper) kend = min(kend, n0 + TBN);
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
   if (tid == 0) {
@@ -440,9 +445,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
       const int s = kt % TSTAGES;
       if (kt >= TSTAGES) mbar_wait(&empty_bar[s], ((kt / TSTAGES) - 1) & 1);
       const int k0 = (int)(kbeg + (int64_t)kt * BK);
-      char* sa = sbase + s * 2 * TILE_BYTES;
+      char* sa = sbase + s * STAGE_BYTES;
       char* sb = sa + TILE_BYTES;
-      mbar_arrive_expect_tx(&full_bar[s], 2 * TILE_BYTES);
+      mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
       if (AK) {
         tma_load_2d(sa, &tp.ta, k0, (int)m0, &full_bar[s]);
       } else {
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
         tma_load_2d(sb, &tp.tb, k0, (int)n0, &full_bar[s]);
       } else {
 #pragma unroll
-        for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, &tp.tb, (int)n0 + 16 * b, k0, &full_bar[s]);
+        for (int b = 0; b < TBN / 16; ++b) tma_load_2d(sb + b * 2048, &tp.tb, (int)n0 + 16 * b, k0, &full_bar[s]);
       }
     }
     return;
@@ -463,36 +468,37 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
   asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
-  double acc[8][4][2];
+  double acc[8][NJ][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % TSTAGES;
     mbar_wait(&full_bar[s], (kt / TSTAGES) & 1);
-    const char* sa = sbase + s * 2 * TILE_BYTES;
-    mma_ktile_sw<AK, BKM>(sa, sa + TILE_BYTES, acc, wm, wn, g, t);
+    const char* sa = sbase + s * STAGE_BYTES;
+    mma_ktile_sw<AK, BKM, NJ>(sa, sa + TILE_BYTES, acc, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
-  epilogue<AK, BKM>(p, acc, tile, z, m0, n0, wm, wn, g, t);
+  epilogue<AK, BKM, NJ>(p, acc, tile, z, m0, n0, wm, wn, g, t);
 }
 
 // Fixed-order split-K reduction + epilogue.  One thread per tile element.
 __global__ void splitk_reduce(Params p) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t tile = idx / (BM * BN);
+  const int bn = p.bn;
+  const int64_t tile = idx / (BM * bn);
   if (tile >= p.ntiles) return;
-  const int e = (int)(idx % (BM * BN));
+  const int e = (int)(idx % (BM * bn));
   const int nl = e / BM, ml = e % BM;
   int bi, bj;
   tile_coords(p, tile, bi, bj);
-  const int64_t m = (int64_t)bi * BM + ml, n = (int64_t)bj * BN + nl;
+  const int64_t m = (int64_t)bi * BM + ml, n = (int64_t)bj * bn + nl;
   if (m >= p.M || n >= p.N) return;
   if (p.sym && m > n) return;
   double s = 0.0;
-  for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * p.ntiles + tile) * (BM * BN) + e];
+  for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * p.ntiles + tile) * (BM * bn) + e];
   double v = p.alpha * s;
   if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
   if (p.row_scale) v *= p.row_scale[m];
@@ -508,12 +514,32 @@ struct Plan {
   int splits;
   int64_t kspan;
   size_t ws_bytes;
+  int bn;
 };
 
-Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
+// Tile width in n for an output of N columns: the width of {128, 96, 64} that pads N the least
+// (ties go to the wider tile).  A chain merge reconstructs N ~ 78-95 (config 2) or ~ 287
+// (config 4) columns: 96-wide tiles are 81-99 % full where 128-wide ones are 61-75 % full; a
+// config-3 leaf's 300 modes take five 64-wide tiles (320) instead of three 128-wide ones (384).
+// Depends on N only, so the plan -- and with it every bit of the result -- is shape-determined.
+int narrow_bn(int64_t N) {
+  int best = BN;
+  int64_t pad = ceil_div(N, (int64_t)BN) * BN;
+  for (int bn : {96, 64}) {
+    const int64_t pd = ceil_div(N, (int64_t)bn) * bn;
+    if (pd < pad) {
+      pad = pd;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = BN) {
   Plan pl;
+  pl.bn = bn;
   pl.tiles_m = (int)ceil_div(M, BM);
-  pl.tiles_n = (int)ceil_div(N, BN);
+  pl.tiles_n = (int)ceil_div(N, (int64_t)bn);
   pl.ntiles = sym ? (int64_t)pl.tiles_m * (pl.tiles_m + 1) / 2 : (int64_t)pl.tiles_m * pl.tiles_n;
   // Split-K only when the output alone cannot fill the chip.  Depends on the
   // shape only (never on the device count) so results are reproducible.
@@ -532,7 +558,7 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
   pl.kspan = ceil_div(ceil_div(K, splits), BK) * BK;
   splits = std::max<int64_t>(1, ceil_div(K, std::max<int64_t>(pl.kspan, 1)));
   pl.splits = (int)splits;
-  pl.ws_bytes = pl.splits > 1 ? (size_t)pl.splits * pl.ntiles * BM * BN * sizeof(double) : 0;
+  pl.ws_bytes = pl.splits > 1 ? (size_t)pl.splits * pl.ntiles * BM * bn * sizeof(double) : 0;
   return pl;
 }
 
@@ -551,8 +577,6 @@ int launch_t(const Params& p, cudaStream_t st) {
   HP_CHECK_LAUNCH("gemm_kernel");
   return HP_OK;
 }
-
-constexpr int TMA_SMEM = TSTAGES * 2 * TILE_BYTES + 1024;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -581,8 +605,10 @@ bool encode_map(CUtensorMap* map, const double* base, int64_t inner, int64_t out
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool AK, bool BKM>
+template <bool AK, bool BKM, int NJ = 4>
 int launch_tma(const Params& p, cudaStream_t st, bool& done) {
+  constexpr int TBN = 32 * NJ;
+  constexpr int SMEM = TSTAGES * (TILE_BYTES + TBN * BK * 8) + 1024;
   done = false;
   static std::atomic<unsigned long long> configured{0};
   TmaParams tp;
@@ -591,17 +617,17 @@ int launch_tma(const Params& p, cudaStream_t st, bool& done) {
   // M-major: inner = M / N (contiguous rows of each k-vector), outer = K, box {16, 16}
   const bool ok_a = AK ? encode_map(&tp.ta, p.A.base, p.K, p.M, p.A.ld, BK, BM)
                        : encode_map(&tp.ta, p.A.base, p.M, p.K, p.A.ld, 16, BK);
-  const bool ok_b = BKM ? encode_map(&tp.tb, p.B.base, p.K, p.N, p.B.ld, BK, BN)
+  const bool ok_b = BKM ? encode_map(&tp.tb, p.B.base, p.K, p.N, p.B.ld, BK, TBN)
                         : encode_map(&tp.tb, p.B.base, p.N, p.K, p.B.ld, 16, BK);
   if (!ok_a || !ok_b) return HP_OK;  // not encodable: caller uses the cp.async kernel
   const int rc0 = once_per_device(configured, []() -> int {
-    HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       TMA_SMEM));
+    HP_CHECK_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM));
     return (int)HP_OK;
   });
   if (rc0 != HP_OK) return rc0;
   dim3 grid((unsigned)p.ntiles, 1, (unsigned)p.splits);
-  gemm_tma_kernel<AK, BKM><<<grid, TTHREADS, TMA_SMEM, st>>>(tp);
+  gemm_tma_kernel<AK, BKM, NJ><<<grid, TTHREADS, SMEM, st>>>(tp);
   HP_CHECK_LAUNCH("gemm_tma_kernel");
   done = true;
   return HP_OK;
@@ -618,7 +644,6 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   HP_REQUIRE(!sym || M == N, "gemm: symmetric output needs M == N");
   if (M == 0 || N == 0) return HP_OK;
   Params p{};
-  Plan pl = make_plan(M, N, K, sym, b_upper);
   p.M = M;
   p.N = N;
   p.K = K;
@@ -633,33 +658,43 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   p.col_div = col_div;
   p.sym = sym;
   p.b_upper = b_upper;
-  p.tiles_m = pl.tiles_m;
-  p.tiles_n = pl.tiles_n;
-  p.ntiles = pl.ntiles;
-  p.splits = pl.splits;
-  p.kspan = pl.kspan;
-  if (pl.splits > 1) {
-    if (ws_bytes < pl.ws_bytes) {
-      // not enough workspace: fall back to a single split (same arithmetic class, one more wave)
-      p.splits = 1;
-      p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
-    } else {
-      p.partial = static_cast<double*>(ws);
+  auto apply_plan = [&](const Plan& pl) {
+    p.bn = pl.bn;
+    p.tiles_m = pl.tiles_m;
+    p.tiles_n = pl.tiles_n;
+    p.ntiles = pl.ntiles;
+    p.splits = pl.splits;
+    p.kspan = pl.kspan;
+    p.partial = nullptr;
+    if (pl.splits > 1) {
+      if (ws_bytes < pl.ws_bytes) {
+        // not enough workspace: fall back to a single split (same arithmetic class, one more wave)
+        p.splits = 1;
+        p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
+      } else {
+        p.partial = static_cast<double*>(ws);
+      }
     }
-  }
-  int rc;
+  };
+  const bool tma_ok = aligned16 && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31);
+  // narrow n tiles (96 / 64 wide) exist on the TMA path with a K-major B operand only
+  const int bn = (tma_ok && b_kmajor && !sym && !b_upper) ? narrow_bn(N) : BN;
+  apply_plan(make_plan(M, N, K, sym, b_upper, bn));
+  int rc = HP_OK;
   bool done = false;
-  rc = HP_OK;
-  if (aligned16 && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31)) {
+  if (tma_ok) {
     if (a_kmajor && b_kmajor)
-      rc = launch_tma<true, true>(p, st, done);
+      rc = bn == 96 ? launch_tma<true, true, 3>(p, st, done)
+                    : bn == 64 ? launch_tma<true, true, 2>(p, st, done) : launch_tma<true, true>(p, st, done);
     else if (!a_kmajor && b_kmajor)
-      rc = launch_tma<false, true>(p, st, done);
+      rc = bn == 96 ? launch_tma<false, true, 3>(p, st, done)
+                    : bn == 64 ? launch_tma<false, true, 2>(p, st, done) : launch_tma<false, true>(p, st, done);
     else if (!a_kmajor && !b_kmajor)
       rc = launch_tma<false, false>(p, st, done);
     else
       rc = launch_tma<true, false>(p, st, done);
   }
+  if (!rc && !done && bn != BN) apply_plan(make_plan(M, N, K, sym, b_upper, BN));  // tensor map not encodable
   if (rc || done) {
   } else if (a_kmajor && b_kmajor)
     rc = aligned16 ? launch_t<true, true, true>(p, st) : launch_t<true, true, false>(p, st);
@@ -671,7 +706,7 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
     rc = aligned16 ? launch_t<true, false, true>(p, st) : launch_t<true, false, false>(p, st);
   if (rc) return rc;
   if (p.splits > 1) {
-    const int64_t total = p.ntiles * BM * BN;
+    const int64_t total = p.ntiles * BM * p.bn;
     splitk_reduce<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(p);
     HP_CHECK_LAUNCH("splitk_reduce");
   }
@@ -680,7 +715,10 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
 
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
   if (M <= 0 || N <= 0) return 0;
-  return gemm::make_plan(M, N, K, sym, b_upper).ws_bytes;
+  size_t need = gemm::make_plan(M, N, K, sym, b_upper).ws_bytes;
+  if (!sym && !b_upper)  // the narrow-tile plan of the same shape (gemm_run picks it on the TMA path)
+    need = std::max(need, gemm::make_plan(M, N, K, sym, b_upper, gemm::narrow_bn(N)).ws_bytes);
+  return need;
 }
 
 }  // namespace hp
