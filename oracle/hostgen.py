@@ -75,14 +75,28 @@ def pulse(d: int, cols: np.ndarray, seed: int) -> np.ndarray:
     return np.asfortranarray(np.exp(-0.5 * z * z))
 
 
+_SINE_COEF: dict = {}
+
+
+def _sine_coefficients(seed: int, nmax: int, modes: int) -> np.ndarray:
+    """Rows 0..nmax-1 of the seeded N(0,1) coefficient stream (drawn row-major, so a prefix does
+    not depend on how many rows are drawn); cached, grown in powers of two."""
+    have = _SINE_COEF.get((seed, modes))
+    if have is None or have.shape[0] < nmax:
+        rows = 1 << max(nmax - 1, 1).bit_length()
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 3])))
+        have = rng.standard_normal((rows, modes))
+        _SINE_COEF[(seed, modes)] = have
+    return have[:nmax]
+
+
 def sine(d: int, cols: np.ndarray, seed: int, noise_key: int = 0, modes: int = 300, noise: float = 1e-8) -> np.ndarray:
     """BASELINE config 3 columns: sum_{k<=300} k^-2 a_jk sin(k pi x) + 1e-8 N(0,1).  The coefficient
     stream is the device generator's; the noise stream is NumPy's (the device draws it with the
     CUDA generator), so these are statistically -- not bytewise -- the device's columns: they
     serve the CPU timing samples of bench.py only."""
-    rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), 3])))
     nmax = int(cols.max()) + 1 if cols.size else 0
-    a = rng.standard_normal((max(nmax, 1), modes))[cols] / (np.arange(1, modes + 1) ** 2)[None, :]
+    a = _sine_coefficients(seed, nmax, modes)[cols] / (np.arange(1, modes + 1) ** 2)[None, :]
     x = np.linspace(0.0, 1.0, d)
     basis = np.sin(np.pi * np.arange(1, modes + 1)[None, :] * x[:, None])  # (d, modes)
     out = basis @ a.T
