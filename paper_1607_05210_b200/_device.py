@@ -128,6 +128,65 @@ def _even(n: int) -> int:
     return n + (n & 1)
 
 
+class Guards:
+    """Debug allocation mode (the pool's substitute for compute-sanitizer memcheck, which is closed
+    here): every matrix (DevMat.empty) and kernel workspace (_ws) is allocated with a 4 KB canary
+    zone on both sides and a poisoned (signalling-pattern NaN) payload.  ``check()`` verifies that
+    no kernel wrote outside its buffer; a kernel that consumes memory it was supposed to have
+    written first propagates the poison NaN into results the tests compare with the oracle.
+    Off by default; used by tests/test_gpu_guards.py."""
+
+    active = False
+    CANARY = 0x7FF8DEADBEEFCAFE   # quiet NaN with a recognisable payload
+    POISON = 0x7FF8BAADF00DBAAD
+    ZONE = 4096                   # bytes on each side
+    _live: list = []
+    _lock = threading.Lock()
+
+    @classmethod
+    def enable(cls):
+        cls._live = []
+        cls.active = True
+
+    @classmethod
+    def disable(cls):
+        cls.active = False
+        cls._live = []
+
+    @classmethod
+    def alloc(cls, n: int, dtype, zero: bool):
+        esz = torch.empty(0, dtype=dtype).element_size()
+        nbytes = n * esz
+        pad = (-nbytes) % 8
+        raw = torch.empty((2 * cls.ZONE + nbytes + pad) // 8, dtype=torch.int64, device="cuda")
+        raw.fill_(cls.POISON)
+        raw[: cls.ZONE // 8] = cls.CANARY
+        raw[(cls.ZONE + nbytes + pad) // 8:] = cls.CANARY
+        payload = raw.view(torch.uint8)[cls.ZONE: cls.ZONE + nbytes].view(dtype)
+        if zero:
+            payload.zero_()
+        with cls._lock:
+            cls._live.append((raw, nbytes + pad))
+        return payload
+
+    @classmethod
+    def check(cls) -> int:
+        """Number of guarded allocations verified; raises if any canary word changed."""
+        torch.cuda.synchronize()
+        want = cls.CANARY
+        with cls._lock:
+            live = list(cls._live)
+        for k, (raw, nbytes) in enumerate(live):
+            head = raw[: cls.ZONE // 8]
+            tail = raw[(cls.ZONE + nbytes) // 8:]
+            if not bool((head == want).all()) or not bool((tail == want).all()):
+                bad_h = int((head != want).sum())
+                bad_t = int((tail != want).sum())
+                raise AssertionError(f"guarded allocation {k} ({nbytes} bytes): {bad_h} canary words overwritten "
+                                     f"before and {bad_t} after the buffer")
+        return len(live)
+
+
 class DevMat:
     """Column-major float64 matrix on the current CUDA device."""
 
@@ -144,8 +203,11 @@ class DevMat:
     def empty(rows: int, cols: int, zero: bool = False):
         ld = max(_even(rows), 2)
         n = max(ld * cols, 1)
-        st = torch.zeros(n, dtype=torch.float64, device="cuda") if zero else \
-            torch.empty(n, dtype=torch.float64, device="cuda")
+        if Guards.active:
+            st = Guards.alloc(n, torch.float64, zero)
+        else:
+            st = torch.zeros(n, dtype=torch.float64, device="cuda") if zero else \
+                torch.empty(n, dtype=torch.float64, device="cuda")
         return DevMat(st, rows, cols, ld)
 
     @property
@@ -168,12 +230,12 @@ class DevMat:
         """(rows, cols) torch view (column-major strides)."""
         if self.cols == 0:
             return torch.zeros((self.rows, 0), dtype=torch.float64, device=self.storage.device)
-        return self.storage.as_strided((self.rows, self.cols), (1, self.ld), self.offset)
+        return self.storage.as_strided((self.rows, self.cols), (1, self.ld), self.storage.storage_offset() + self.offset)
 
     def to_numpy(self) -> np.ndarray:
         if self.cols == 0 or self.rows == 0:
             return np.zeros((self.rows, self.cols))
-        t = self.storage.as_strided((self.cols, self.rows), (self.ld, 1), self.offset)
+        t = self.storage.as_strided((self.cols, self.rows), (self.ld, 1), self.storage.storage_offset() + self.offset)
         host = t.cpu().numpy()  # (cols, rows) C-order == (rows, cols) F-order
         return np.asfortranarray(host.T)
 
@@ -408,6 +470,8 @@ def weigh_parts(parts: list[Part], sqrt_w) -> list[Part]:
 
 
 def _ws(nbytes: int):
+    if Guards.active:
+        return Guards.alloc(max(int(nbytes), 16), torch.uint8, False)
     return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
 
 

@@ -1,0 +1,94 @@
+"""BASELINE configs 3 and 4 at their REAL tree shapes (reduced rows) against committed fixtures
+of the unmodified reference (tests/golden/make_tree_fixture.py):
+
+  config 3: star(64) of 512-column leaves + the ~19,000-column root   (hierarchy.py:323-367)
+  config 4: 8 chains of 16 slices under one root, zero leaf tolerance (hierarchy.py:182-222)
+
+The snapshots are regenerated on this host with oracle/hostgen.py (NumPy Philox; compared with
+the fixture through hostgen.checksum), uploaded, and the device tree runs through the public
+API.  Asserted: every node's input/output counts identical; every kept sigma, the principal
+angles to the reference's modes and the projection l2 within max(BASELINE gate, 4 x the
+fixture's CPU-vs-CPU floor); the a-priori bound and eps* respected.
+"""
+
+import importlib.util
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1607_05210_b200 as H  # noqa: E402
+from oracle import hapod_oracle as O  # noqa: E402
+from oracle import hostgen  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+_spec = importlib.util.spec_from_file_location("make_tree_fixture", os.path.join(GOLD, "make_tree_fixture.py"))
+MTF = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(MTF)
+
+K_FLOOR = 4.0
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config_tree_real_shape_vs_reference_fixture(cfg):
+    npz = os.path.join(GOLD, f"c{cfg}_tree.npz")
+    if not os.path.exists(npz):
+        pytest.skip(f"c{cfg} tree fixture not generated")
+    fix = np.load(npz)
+    with open(os.path.join(GOLD, f"c{cfg}_tree.json")) as f:
+        meta = json.load(f)
+    ref = meta["reference"]
+    sp = MTF.SPEC[cfg]
+    s = MTF.snapshots(cfg)
+    d, m = s.shape
+    assert (d, m) == (ref["d"], ref["m"])
+    chk = hostgen.checksum(s)
+    assert np.max(np.abs(chk - fix["checksum"])) <= 1e-9 * max(1.0, float(np.abs(fix["checksum"]).max()))
+    fro = float(np.linalg.norm(s))
+    assert fro == pytest.approx(ref["fro"], rel=1e-12)
+    eps_star = sp["rel"] * fro
+    target = H.eps_star_to_target(eps_star, m)
+
+    children = MTF.tree_children(cfg)
+    tree = H.RootedTree(tuple(tuple(c) for c in children), 0)
+    assert list(H.derive_maps(tree).leaf_order) == MTF.dfs_leaves(children)
+    space = H.InnerProductSpace(d)
+    blk = H.SnapshotBlock(space, s)
+    leaves = H.distribute_columns(tree, blk, block_size=sp["block"])
+    tol = H.assign_tolerances(tree, leaves, target, omega=sp["omega"], zero_leaf_tolerance=(cfg == 4))
+    np.testing.assert_allclose(np.asarray(tol.epsilons), np.asarray(ref["epsilons"]), rtol=1e-12, atol=0.0)
+    res = H.run_hapod(tree, leaves, tol)
+
+    ref_rep = {r["node"]: r for r in ref["reports"]}
+    mism = [(r.node, r.input_count, r.output_mode_count, ref_rep[r.node]["n_in"], ref_rep[r.node]["n_out"])
+            for r in res.reports
+            if (r.output_mode_count, r.input_count) != (ref_rep[r.node]["n_out"], ref_rep[r.node]["n_in"])]
+    sig = np.asarray(res.modes.sigmas)
+    modes = np.asarray(res.modes.modes)
+    rsig, rmodes = fix["sigmas"], fix["modes"]
+    n = min(len(sig), len(rsig))
+    rel = np.abs(sig[:n] - rsig[:n]) / rsig[:n]
+    ang = O.principal_angle_sines(modes, rmodes) if len(sig) == len(rsig) else np.array([np.inf])
+    err = math.sqrt(H.actual_mean_error(blk, res.modes) * m)
+    fl = meta["floor"]
+    interior = [r.output_mode_count for r in res.reports if not r.is_leaf]
+    print(f"\n[c{cfg} real tree shape d'={d}, {len(children)} nodes] root modes gpu={len(sig)} reference={len(rsig)}; "
+          f"node-count mismatches {len(mism)}; interior outputs {min(interior)}-{max(interior)}; "
+          f"max rel dsigma {rel.max():.3e} (CPU floor {fl['rel_dsigma']:.3e}); max angle sine {ang.max():.3e} "
+          f"(CPU floor {fl['angle']:.3e}); l2 gpu {err:.8e} reference {ref['l2']:.8e} (rel diff "
+          f"{abs(err - ref['l2']) / ref['l2']:.2e}, CPU floor {fl['l2_rel']:.2e}); eps* {eps_star:.6e}")
+    assert not mism, mism[:5]
+    assert len(sig) == ref["N"]
+    assert rel.max() <= max(1e-10, K_FLOOR * fl["rel_dsigma"])
+    assert ang.max() <= max(1e-8, K_FLOOR * fl["angle"])
+    assert abs(err - ref["l2"]) <= max(1e-8, K_FLOOR * fl["l2_rel"]) * ref["l2"]
+    assert err <= eps_star
+    assert res.apriori_error_bound == pytest.approx(ref["apriori"], rel=1e-12)
