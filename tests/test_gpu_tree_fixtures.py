@@ -89,6 +89,11 @@ def test_config_tree_real_shape_vs_reference_fixture(cfg):
     assert len(sig) == ref["N"]
     assert rel.max() <= max(1e-10, K_FLOOR * fl["rel_dsigma"])
     assert ang.max() <= max(1e-8, K_FLOOR * fl["angle"])
-    assert abs(err - ref["l2"]) <= max(1e-8, K_FLOOR * fl["l2_rel"]) * ref["l2"]
+    # l2: 1e-8 relative, or 4x the CPU floor, or -- where the residual sits at the noise level (config 3:
+    # l2 = 1.2e-8 ||S||_F) -- the accuracy to which ANY fp64 evaluation of ||S - U U^T S||_F is defined:
+    # inner products of length d and N carry (sqrt(d) + sqrt(N)) u ||S||_F of rounding (8x margin)
+    eval_floor = 8.0 * (math.sqrt(d) + math.sqrt(len(sig))) * 2.0 ** -53 * fro
+    print(f"[c{cfg}] l2 evaluation floor {eval_floor:.2e} absolute = {eval_floor / ref['l2']:.2e} relative")
+    assert abs(err - ref["l2"]) <= max(max(1e-8, K_FLOOR * fl["l2_rel"]) * ref["l2"], eval_floor)
     assert err <= eps_star
     assert res.apriori_error_bound == pytest.approx(ref["apriori"], rel=1e-12)
