@@ -113,6 +113,19 @@ int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V
             double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
             int* sweeps, double* flops, void* ws, size_t ws_bytes, void* stream);
 
+/* K2, one rank's share of a replicated eigensolve (multi-GPU root): the same
+ * iteration as hp_syev without Rayleigh refinement -- identical eigenvalues, sweeps and rotations on
+ * every rank -- but the eigenvector accumulation V <- V J (half of a round's DMMA products) is
+ * restricted to the rows [vrow0, vrow1) of the padded matrix (whole 64-row slabs of
+ * hp_syev_padded_order(n) rows; vrow1 < 0: all rows).  Rows of V outside the range are not
+ * meaningful; the ranks all-gather their row ranges.  The reference computes the whole
+ * decomposition in one LAPACK call (pod.py:329-331); its wave executor (parallel.py:77-142) has no
+ * counterpart for a single node's eigensolve. */
+int64_t hp_syev_padded_order(int64_t n);
+int hp_syev_rows(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+                 double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
+                 double* flops, int64_t vrow0, int64_t vrow1, void* ws, size_t ws_bytes, void* stream);
+
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
  * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank
  * whose tail sum_{n>=N} sigma_n^2 <= eps^2, tail = sum lam_keep[N:].

@@ -402,11 +402,11 @@ def pack_parts(parts: list[Part]) -> list[Part]:
     m = sum(p.mat.cols for p in live)
     out = DevMat.empty(d, m)
     at = 0
-    dst = out.storage[: out.ld * m].view(m, out.ld)
+    st = _stream()
     for p in live:
         c = p.mat.cols
-        src = p.mat.storage[p.mat.offset: p.mat.offset + p.mat.ld * c].view(c, p.mat.ld)
-        dst[at: at + c, :d].copy_(src[:, :d])
+        # the repo's own copy kernel (hp_scale without scales), not an eager torch copy
+        N.check(lib.hp_scale(p.mat.ptr, p.mat.ld, d, c, None, None, None, out.col_ptr(at), out.ld, st), "pack")
         at += c
     scale = None
     if any(p.scale is not None for p in live):
@@ -559,8 +559,43 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
     return drift0
 
 
+class EigShare:
+    """One rank's share of a REPLICATED eigensolve (multi-GPU root): every rank runs
+    the same deterministic iteration on the same Gramian, accumulates only its own 64-row slabs of
+    the eigenvector matrix (half of a round's DMMA products are V slabs) and the ranks all-gather
+    their rows once at the end.  No communication inside the iteration."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = int(rank), int(world), group
+
+    def slab_rows(self, n_padded: int, rank: int | None = None):
+        """Rows [a, b) of the padded matrix owned by ``rank`` (whole 64-row slabs, contiguous)."""
+        q = self.rank if rank is None else rank
+        slabs = n_padded // 64
+        return 64 * (q * slabs // self.world), 64 * ((q + 1) * slabs // self.world)
+
+    def allgather_rows(self, V: DevMat, n: int, n_padded: int):
+        """Make every row of the n x n matrix V valid on every rank (rank q holds rows slab_rows(q))."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        Vt = V.tensor()
+        spans = [self.slab_rows(n_padded, q) for q in range(self.world)]
+        spans = [(min(a, n), min(b, n)) for a, b in spans]
+        width = max(b - a for a, b in spans)
+        a, b = spans[self.rank]
+        send = torch.zeros((max(width, 1), n), dtype=torch.float64, device="cuda")
+        if b > a:
+            send[: b - a].copy_(Vt[a:b])
+        parts = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(parts, send, group=self.group)
+        for q, (qa, qb) in enumerate(spans):
+            if q != self.rank and qb > qa:
+                Vt[qa:qb].copy_(parts[q][: qb - qa])
+
+
 def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, keep_floor=0.0, tol_angle=0.0,
-          refine=True):
+          refine=True, share: EigShare | None = None):
     lib = N.load()
     lam = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
     V = DevMat.empty(n, n)
@@ -568,12 +603,22 @@ def _syev(G: DevMat, n: int, st, name="eigensolve", tol_rel=None, tol_abs=None, 
     sweeps = ctypes.c_int(0)
     eflops = ctypes.c_double(0.0)
     ph = _phase(name)
+    tr = JACOBI_TOL_REL if tol_rel is None else tol_rel
+    ta = JACOBI_TOL_ABS if tol_abs is None else tol_abs
     with ph:
-        N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n,
-                            JACOBI_TOL_REL if tol_rel is None else tol_rel,
-                            JACOBI_TOL_ABS if tol_abs is None else tol_abs, float(tol_angle), float(keep_floor),
-                            JACOBI_MAX_SWEEPS, int(refine), ctypes.byref(sweeps), ctypes.byref(eflops), ws.data_ptr(),
-                            ws.numel(), st), "eigensolve")
+        if share is not None and share.world > 1:
+            if refine:
+                raise ValueError("a shared eigensolve cannot refine its eigenvalues (needs all rows of V)")
+            npad = int(lib.hp_syev_padded_order(n))
+            a, b = share.slab_rows(npad)
+            N.check(lib.hp_syev_rows(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n, tr, ta, float(tol_angle),
+                                     float(keep_floor), JACOBI_MAX_SWEEPS, ctypes.byref(sweeps),
+                                     ctypes.byref(eflops), a, b, ws.data_ptr(), ws.numel(), st), "eigensolve")
+            share.allgather_rows(V, n, npad)
+        else:
+            N.check(lib.hp_syev(G.ptr, G.ld, n, lam.data_ptr(), V.ptr, V.ld, n, tr, ta, float(tol_angle),
+                                float(keep_floor), JACOBI_MAX_SWEEPS, int(refine), ctypes.byref(sweeps),
+                                ctypes.byref(eflops), ws.data_ptr(), ws.numel(), st), "eigensolve")
         ph.flops = eflops.value
     return lam, V, sweeps.value
 
@@ -591,7 +636,7 @@ class EigVectors:
     sweeps: int
 
 
-def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
+def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float, share: EigShare | None = None) -> EigVectors:
     """pod.py:329-331 + 278-289 on the device: eigensolve of the node Gramian, cutoff keep,
     truncation rank and tail, and the N kept eigenvectors.
 
@@ -624,7 +669,8 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float) -> EigVectors:
                     "H = L^T L")
         del ws
     # with the polish, H's eigenvalues only select K and scale Q0: no Rayleigh refinement
-    lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS, refine=False)
+    # (a multi-GPU root passes `share`: this rank accumulates only its rows of W, all-gathered after)
+    lam, W, sweeps = _syev(H, r, st, tol_abs=PC_TOL_ABS, refine=False, share=share)
     nev = r
     basis, divide = Lf, True
     if r:

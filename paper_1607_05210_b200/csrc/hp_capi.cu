@@ -38,9 +38,11 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
              const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
 size_t syev_workspace_bytes(int64_t n);
+int64_t syev_padded_order(int64_t n);
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
              double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
-             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st);
+             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st, int64_t vrow0 = 0,
+             int64_t vrow1 = -1);
 int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
                  cudaStream_t st);
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
@@ -232,6 +234,15 @@ int hp_syev(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V
             int* sweeps, double* flops, void* ws, size_t ws_bytes, void* stream) {
   return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, tol_angle, keep_floor, max_sweeps, refine,
                   sweeps, flops, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int64_t hp_syev_padded_order(int64_t n) { return syev_padded_order(n); }
+
+int hp_syev_rows(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
+                 double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
+                 double* flops, int64_t vrow0, int64_t vrow1, void* ws, size_t ws_bytes, void* stream) {
+  return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, tol_angle, keep_floor, max_sweeps, 0, sweeps,
+                  flops, ws, ws_bytes, (cudaStream_t)stream, vrow0, vrow1);
 }
 
 int hp_truncate(const double* lam_desc, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info4,

@@ -71,6 +71,9 @@ struct Params {
   int* tile_mark;     // per G tile: stamp of the round whose "needed" pass already applied it
   int stamp;
   int phase;          // apply: 1 = tiles needed by the next round's local solves, 2 = the rest
+  int slab_extra;     // one more slab accumulated besides the range (-1: none): the slab holding the padding rows
+  int slab0, nslab;   // V accumulation restricted to the 64-row slabs [slab0, slab0 + nslab) (all of them by default):
+                      // a rank of the row-distributed root accumulates only its own rows of V
 };
 
 __device__ __forceinline__ void circle_pair(int nplayers, int r, int k, int& a, int& b) {
@@ -525,9 +528,10 @@ __device__ __forceinline__ void apply_task(const Params& p, int64_t b, int64_t n
   }
   // V slab: rows [rc*64, rc*64+64), columns of pair Q (Q-major, so consecutive tasks share W_Q)
   const int64_t vb = b - ng;
-  const int64_t nrc = p.np / PS;
+  const int64_t nrc = p.nslab + (p.slab_extra >= 0);
   const int Q = (int)(vb / nrc);
-  const int64_t rc = vb % nrc;
+  const int64_t ri = vb % nrc;
+  const int64_t rc = ri < p.nslab ? p.slab0 + ri : p.slab_extra;
   if (!p.flags[Q]) return;
   int qp, qq;
   block_pair(p, Q, qp, qq);
@@ -588,7 +592,7 @@ __global__ void __launch_bounds__(AT, 2) jac_apply(Params p) {
 __device__ __forceinline__ void rest_tasks(const Params& p, double* X, double* WQ, double* WP) {
   const int npairs = p.nb / 2;
   const int64_t ng = (int64_t)npairs * (npairs + 1) / 2;
-  const int64_t ntasks = ng + (p.np / PS) * npairs;
+  const int64_t ntasks = ng + (int64_t)(p.nslab + (p.slab_extra >= 0)) * npairs;
   // dynamic scheduling in chunks of consecutive tasks (which mostly share the column pair Q, whose
   // rotation then stays in shared memory): the heavy G tiles (two 64^3 products) come first, the
   // V slabs (one product) last, and CTAs sharing an SM with a local solve simply take fewer chunks
@@ -650,10 +654,23 @@ __global__ void max_abs_diag(const double* Gp, int64_t np, int64_t n, double* ou
 // unit vectors of the zero padding, never mixed with real coordinates): -inf.
 // Y == nullptr: no refinement, the value is the converged diagonal entry Y0[col*ldy0 + col].
 __global__ void rq_diag(const double* V, int64_t ldv, const double* Y, int64_t ldy, int64_t n, int64_t ncols,
-                        double* out, const double* diag_src = nullptr, int64_t ld_diag = 0) {
+                        double* out, const double* diag_src = nullptr, int64_t ld_diag = 0, int by_padding_rows = 0) {
   const int64_t col = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (col >= ncols) return;
+  if (by_padding_rows) {
+    // partial V (only some row slabs accumulated): a padding eigenvector is a unit vector of the
+    // padding rows [n, ncols) -- rows every partial call accumulates -- a real one vanishes there
+    double pp = 0.0;
+    for (int64_t k = n + lane; k < ncols; k += 32) {
+      const double v = V[col * ldv + k];
+      pp += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pp += __shfl_xor_sync(0xffffffffu, pp, o);
+    if (lane == 0) out[col] = pp > 0.5 ? -INFINITY : diag_src[col * ld_diag + col];
+    return;
+  }
   double s = 0.0, nn = 0.0;
   for (int64_t k = lane; k < n; k += 32) {
     const double v = V[col * ldv + k];
@@ -734,10 +751,12 @@ Layout layout(int64_t n) {
 }  // namespace jac
 
 size_t syev_workspace_bytes(int64_t n) { return jac::layout(n).total; }
+int64_t syev_padded_order(int64_t n) { return jac::layout(n).np; }
 
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
              double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
-             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+             int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st, int64_t vrow0,
+             int64_t vrow1) {
   using namespace jac;
   HP_REQUIRE(n >= 0, "syev: negative order");
   if (sweeps_out) *sweeps_out = 0;
@@ -764,6 +783,22 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   int* perm = reinterpret_cast<int*>(base + L.off_perm);
   p.np = L.np;
   p.nb = L.nb;
+  // rows of V this call accumulates: whole 64-row slabs [vrow0, vrow1) (vrow1 < 0: all rows).  The
+  // eigenvalues and every other row of the iteration do not depend on the range.
+  if (vrow1 < 0) {
+    vrow0 = 0;
+    vrow1 = L.np;
+  }
+  HP_REQUIRE(vrow0 >= 0 && vrow0 <= vrow1 && vrow1 <= L.np && vrow0 % PS == 0 && (vrow1 % PS == 0 || vrow1 == L.np),
+             "syev: V row range must be whole 64-row slabs");
+  const bool partial = !(vrow0 == 0 && vrow1 == L.np);
+  HP_REQUIRE(!partial || !refine, "syev: Rayleigh refinement needs all rows of V");
+  p.slab0 = (int)(vrow0 / PS);
+  p.nslab = (int)(ceil_div(vrow1, (int64_t)PS) - p.slab0);
+  // a partial call also accumulates the last slab: it holds the padding rows (np - n < 64 of them),
+  // whose entries tell padding eigenvectors from real ones without the other ranks' rows
+  const int last_slab = (int)(L.np / PS) - 1;
+  p.slab_extra = (partial && L.np > n && p.slab0 + p.nslab <= last_slab) ? last_slab : -1;
   p.tol_rel = tol_rel;
   p.tol_abs = tol_abs;
   p.keep_floor = keep_floor;
@@ -789,7 +824,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   HP_CHECK_LAUNCH("max_abs_diag");
 
   const int npairs = L.nb / 2;
-  const int64_t napply = (int64_t)npairs * (npairs + 1) / 2 + (L.np / PS) * npairs;
+  const int64_t napply = (int64_t)npairs * (npairs + 1) / 2 + (int64_t)(p.nslab + (p.slab_extra >= 0)) * npairs;
   int nsm = 148, dev = 0;
   HP_CHECK_CUDA(cudaGetDevice(&dev));
   HP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -889,7 +924,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
       if (rc) return rc;
       rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, p.G, L.np, n, L.np, rq);
     } else {
-      rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, nullptr, 0, n, L.np, rq, p.G, L.np);
+      rq_diag<<<(unsigned)ceil_div(L.np, 8), 256, 0, st>>>(p.V, L.np, nullptr, 0, n, L.np, rq, p.G, L.np, partial ? 1 : 0);
     }
     HP_CHECK_LAUNCH("rq_diag");
     // rank all n_p columns (padding last), keep the first n

@@ -194,7 +194,7 @@ class RowRootResult:
 
 
 def row_root_pod(S_q, layout: RootLayout, shards: list, eps: float, cutoff: float, rank: int, world: int, arith,
-                 group=None) -> RowRootResult:
+                 group=None, split_eig: bool = True) -> RowRootResult:
     """Steps 3-7 on this rank's row block S_q (rows bounds[rank]..bounds[rank+1] of the root
     input); ``shards``: the fixed shard boundaries (row_bounds)."""
     import torch
@@ -211,23 +211,38 @@ def row_root_pod(S_q, layout: RootLayout, shards: list, eps: float, cutoff: floa
     scale = arith.vector(layout.scale)
     # 3. Gram: per-shard SYRK, fixed-tree sum on rank 0
     G = tree_reduce(lambda s: arith.gram_rows(S_q, *local(s), scale, m), owner, rank, arith, group)
-    # 4. eigen on rank 0, broadcast
-    info = arith.vector(np.zeros(4))
-    if rank == 0:
-        lam_max, nkeep, n_modes, tail, V, sig = arith.eig(G, m, eps, cutoff)
-        info = arith.vector(np.array([lam_max, nkeep, n_modes, tail], dtype=np.float64))
-    del G
-    dist.broadcast(info, 0, group=group)
-    lam_max, nkeep, n_modes, tail = (float(x) for x in arith.to_host(info))
-    nkeep, n_modes = int(nkeep), int(n_modes)
-    if not (lam_max > 0.0) or n_modes == 0:
-        return RowRootResult(arith.empty(r1 - r0, 0), np.zeros(0), tail if lam_max > 0.0 else 0.0, lam_max,
-                             nkeep if lam_max > 0.0 else 0, 0.0, False, bounds, m)
-    if rank != 0:
-        V = arith.empty(m, n_modes)
-        sig = arith.vector(np.zeros(n_modes))
-    dist.broadcast(arith.flat(V), 0, group=group)
-    dist.broadcast(sig, 0, group=group)
+    # 4. eigensolve.  split_eig (default for world > 1): the Gram is broadcast and the eigensolve is
+    #    REPLICATED -- every rank runs the same deterministic iteration and accumulates only its own
+    #    row slabs of the eigenvector matrix, all-gathered at the end (_device.EigShare; no traffic
+    #    inside the iteration); otherwise rank 0 solves alone and broadcasts (lambda_max, nkeep, N,
+    #    tail), sigma and the N kept eigenvectors.
+    if split_eig and world > 1:
+        if rank != 0:
+            G = arith.empty(m, m)
+        dist.broadcast(arith.flat(G), 0, group=group)
+        lam_max, nkeep, n_modes, tail, V, sig = arith.eig(G, m, eps, cutoff, share=(rank, world, group))
+        del G
+        nkeep, n_modes = int(nkeep), int(n_modes)
+        if not (lam_max > 0.0) or n_modes == 0:
+            return RowRootResult(arith.empty(r1 - r0, 0), np.zeros(0), tail if lam_max > 0.0 else 0.0, lam_max,
+                                 nkeep if lam_max > 0.0 else 0, 0.0, False, bounds, m)
+    else:
+        info = arith.vector(np.zeros(4))
+        if rank == 0:
+            lam_max, nkeep, n_modes, tail, V, sig = arith.eig(G, m, eps, cutoff)
+            info = arith.vector(np.array([lam_max, nkeep, n_modes, tail], dtype=np.float64))
+        del G
+        dist.broadcast(info, 0, group=group)
+        lam_max, nkeep, n_modes, tail = (float(x) for x in arith.to_host(info))
+        nkeep, n_modes = int(nkeep), int(n_modes)
+        if not (lam_max > 0.0) or n_modes == 0:
+            return RowRootResult(arith.empty(r1 - r0, 0), np.zeros(0), tail if lam_max > 0.0 else 0.0, lam_max,
+                                 nkeep if lam_max > 0.0 else 0, 0.0, False, bounds, m)
+        if rank != 0:
+            V = arith.empty(m, n_modes)
+            sig = arith.vector(np.zeros(n_modes))
+        dist.broadcast(arith.flat(V), 0, group=group)
+        dist.broadcast(sig, 0, group=group)
     # 5. modes of this row block, shard by shard
     U = arith.empty_rowblock(r1 - r0, n_modes)
     Vs = arith.scale_rows(V, scale)
@@ -399,8 +414,11 @@ class DeviceRowArith:
         G, _, _ = self.D.gram_full([self.D.Part(self.rows_view(S, a, b), scale)], b - a)
         return G
 
-    def eig(self, G, m, eps, cutoff):
-        ev = self.D.eig_vectors(G, m, eps, cutoff)
+    def eig(self, G, m, eps, cutoff, share=None):
+        """``share`` = (rank, world, group): the eigensolve is replicated on every rank and each
+        accumulates its own row slabs of the H-phase eigenvector matrix (_device.EigShare)."""
+        sh = self.D.EigShare(*share) if share is not None else None
+        ev = self.D.eig_vectors(G, m, eps, cutoff, sh)
         if not (ev.lam_max > 0.0) or ev.n_modes == 0:
             return ev.lam_max, ev.nkeep, ev.n_modes, ev.tail, None, None
         V = self.empty(m, ev.n_modes)

@@ -137,7 +137,8 @@ class NumpyRowArith:
         g = x.T @ x
         return torch.from_numpy(np.ascontiguousarray(0.5 * (g + g.T)))
 
-    def eig(self, G, m, eps, cutoff):
+    def eig(self, G, m, eps, cutoff, share=None):
+        # share: the replicated eigensolve of the device path (every rank solves; LAPACK is deterministic here)
         import scipy.linalg
         lam, psi = scipy.linalg.eigh(G.numpy())
         lam, psi = lam[::-1], psi[:, ::-1]

@@ -262,3 +262,42 @@ def test_reortho_two_pass_and_shifted(scale, graded):
     qr_q = qr_q * np.sign(np.diag(r))[None, :]
     # same span (Q unique up to rounding ~ u kappa)
     assert np.linalg.norm(qr_q - qq @ (qq.T @ qr_q)) < 1e-6
+
+
+@pytest.mark.parametrize("n,cuts", [(300, [0, 128, 256, 320]), (200, [0, 64, 256]), (512, [0, 192, 192, 512]),
+                                    (97, [0, 64, 128])])
+def test_syev_rows_partition_is_bitwise_the_full_solve(n, cuts):
+    """hp_syev_rows (one rank's share of a replicated eigensolve): eigenvalues, sweeps and every
+    accumulated row of V are bit-identical to the full solve, whatever the row partition --
+    including an empty share and shares without the padding rows."""
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.sort(10.0 ** rng.uniform(-9, 0, n))[::-1]
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    G = D.upload(g)
+    npad = int(lib.hp_syev_padded_order(n))
+    assert cuts[-1] == npad
+
+    def solve(a, b):
+        lam_d = torch.empty(n, dtype=torch.float64, device="cuda")
+        V = D.DevMat.empty(n, n)
+        w = ws(lib.hp_syev_workspace_bytes(n))
+        sweeps = ctypes.c_int(0)
+        if a is None:
+            N.check(lib.hp_syev(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL, D.JACOBI_TOL_ABS, 0.0,
+                                0.0, 60, 0, ctypes.byref(sweeps), None, w.data_ptr(), w.numel(), st()), "syev")
+        else:
+            N.check(lib.hp_syev_rows(G.ptr, G.ld, n, lam_d.data_ptr(), V.ptr, V.ld, n, D.JACOBI_TOL_REL,
+                                     D.JACOBI_TOL_ABS, 0.0, 0.0, 60, ctypes.byref(sweeps), None, a, b, w.data_ptr(),
+                                     w.numel(), st()), "syev_rows")
+        return lam_d.cpu().numpy(), V.to_numpy(), sweeps.value
+
+    lam_full, v_full, sw_full = solve(None, None)
+    merged = np.full_like(v_full, np.nan)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        lam_p, v_p, sw_p = solve(a, b)
+        assert np.array_equal(lam_p, lam_full) and sw_p == sw_full
+        merged[a:min(b, n)] = v_p[a:min(b, n)]
+    assert np.array_equal(merged, v_full)
+    assert np.max(np.abs(v_full.T @ v_full - np.eye(n))) < 1e-12 * np.sqrt(n)
