@@ -27,9 +27,9 @@ cpu_baseline / --impl reference: the reference algorithm (the oracle port of hap
          ~12 h.  ``cpu_baseline.sample`` states the instance exactly; the b200
          arm runs the SAME instance on the GPU and reports it as ``like_for_like``.
 
---gpus N (N > 1) without a torchrun environment re-launches this script under
-``python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1``
-(one process per GPU, NCCL, ``NCCL_DEBUG=INFO`` so the init lines show the rank count).
+--gpus N (N > 1) without a torchrun environment starts N ranks of this script itself (one process
+per GPU with RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR=127.0.0.1 set as torchrun would, NCCL,
+``NCCL_DEBUG=INFO`` so the init lines show the rank count); under torchrun it uses the given ranks.
 Leaves are placed on ranks in contiguous chunks, child -> parent edges move sigma-scaled mode
 blocks with grouped NCCL send/recv, a star's root is evaluated on row blocks by all ranks
 (rowroot.py); timing is the max over ranks of CUDA-event durations.  Config 2 (one chain)
@@ -93,6 +93,9 @@ def parse():
                          "children's modes on rank 0 (gather)")
     ap.add_argument("--protocol-check", action="store_true",
                     help="CPU rehearsal of the multi-rank launch/edge path (gloo + oracle arithmetic)")
+    ap.add_argument("--shared-gpu-check", action="store_true",
+                    help="rehearsal of the N > 1 DEVICE path with all ranks on cuda:0 over gloo (host-staged "
+                         "tensors, tests/_gloo_cuda_shim.py); a correctness check of the bench path, not a measurement")
     return ap.parse_args()
 
 
@@ -129,7 +132,7 @@ def visible_gpus() -> int:
 def self_launch(a) -> int:
     """--gpus N outside torchrun: start N ranks of this script (one per GPU) and pass the
     exit code through.  Rank 0 prints the JSON line."""
-    if not a.protocol_check and a.impl == "b200":
+    if not a.protocol_check and not a.shared_gpu_check and a.impl == "b200":
         have = visible_gpus()
         if have < a.gpus:
             print(json.dumps({"metric": METRIC, "n_gpus": a.gpus, "error": f"--gpus {a.gpus} needs {a.gpus} visible "
@@ -139,9 +142,33 @@ def self_launch(a) -> int:
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // a.gpus)))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.run(cmd, env=env).returncode
+    # one process per GPU with the torchrun environment (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*), started
+    # directly: torch.distributed.run's own option parser takes abbreviated script flags (e.g. --d) for its own
+    env.update(WORLD_SIZE=str(a.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()),
+               LOCAL_WORLD_SIZE=str(a.gpus))
+    procs = []
+    for r in range(a.gpus):
+        e = dict(env, RANK=str(r), LOCAL_RANK=str(r))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=e))
+    rc = 0
+    try:
+        pending = list(procs)
+        while pending:
+            for p in list(pending):
+                code = p.poll()
+                if code is None:
+                    continue
+                pending.remove(p)
+                if code != 0 and rc == 0:      # one rank failed: stop the others instead of hanging in a collective
+                    rc = code
+                    for q in pending:
+                        q.terminate()
+            time.sleep(0.2)
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    return rc
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -500,8 +527,16 @@ def run_b200(a, world, rank, local):
     import torch
     import torch.distributed as dist
 
+    if a.shared_gpu_check:
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and a.shared_gpu_check:
+        import datetime
+        dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=300))
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import _gloo_cuda_shim
+        _gloo_cuda_shim.install()
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         print(f"[bench] rank {rank}/{world} on cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr,
               flush=True)
@@ -524,7 +559,10 @@ def run_b200(a, world, rank, local):
         if world > 1:
             dist.barrier()
     if rank == 0 and line is not None:
-        if world > 1:
+        if world > 1 and a.shared_gpu_check:
+            line["metric"] = "shared-gpu-check (NOT a measurement: all ranks time-slice one GPU over gloo)"
+            line["comm"] = {"backend": "gloo", "nranks": dist.get_world_size()}
+        elif world > 1:
             line["comm"] = {"backend": "nccl", "nranks": dist.get_world_size(),
                             "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
         print(json.dumps(line), flush=True)
