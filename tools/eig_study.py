@@ -1,8 +1,9 @@
 """Root-node eigensolver study: one config-1-root-like POD (m columns, reduced d) with the
-node phases timed on the launching stream.  Environment knobs (HP_JACOBI_TRACE=2,
-HP_JACOBI_LOCAL_SWEEPS, HP_JACOBI_FUSED, ...) are read by the library.
+node phases timed on the launching stream.  Per-sweep traces come from the explicit debug API
+(``hp_set_debug``, include/hapod_b200.h; the library reads no environment variables): pass a
+flag mask as the 4th argument (1 = per-sweep trace, 2 = mid-round timing).
 
-    python tools/eig_study.py [d] [m] [repeats]
+    python tools/eig_study.py [d] [m] [repeats] [debug flags]
 """
 import os
 import sys
@@ -18,6 +19,9 @@ from paper_1607_05210_b200 import workloads as W  # noqa: E402
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+if len(sys.argv) > 4:
+    from paper_1607_05210_b200 import _native as N  # noqa: E402
+    N.load().hp_set_debug(int(sys.argv[4]))
 wl = W.make(1, d=d, m=m)
 blk = H.SnapshotBlock(H.InnerProductSpace(d), wl.values)
 eps = 0.75 * wl.eps_star
