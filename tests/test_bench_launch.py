@@ -57,3 +57,31 @@ def test_reference_arm_is_host_only_and_labels_its_sample():
     import bench
     a = type("A", (), {"config": 1, "d": None})()
     assert line["config"] == bench.static_config(a)
+
+
+def test_reference_arm_under_torchrun_runs_on_rank0_only():
+    """N > 1: rank 0 alone runs and prints the reference line; the other ranks exit 0 without work."""
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29999")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                       capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert p.returncode == 0 and p.stdout.strip() == ""
+    env["RANK"] = env["LOCAL_RANK"] = "0"
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "0", "--ref-d", "500", "--ref-leaf-cols", "6"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-1500:]
+    line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+
+
+def test_gpus_more_than_visible_is_refused_loudly():
+    """--gpus N on a box with fewer GPUs must not silently run on one: an error line and a non-zero exit."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64"], capture_output=True, text=True,
+                       timeout=120, env=env, cwd=ROOT)
+    assert p.returncode == 2
+    line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][0])
+    assert "error" in line and line["n_gpus"] == 64
