@@ -10,7 +10,7 @@ mkdir -p "$OBJ"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
        -Xptxas -warn-spills -I"$HERE/include")
 pids=()
-for f in hp_gemm hp_jacobi hp_podops hp_pstrf hp_capi; do
+for f in hp_gemm hp_jacobi hp_podops hp_pstrf hp_tridiag hp_capi; do
   "$NVCC" "${FLAGS[@]}" -c "$SRC/$f.cu" -o "$OBJ/$f.o" &
   pids+=($!)
 done

@@ -126,6 +126,24 @@ int hp_syev_rows(const double* G, int64_t ldg, int64_t n, double* lam_desc, doub
                  double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int* sweeps,
                  double* flops, int64_t vrow0, int64_t vrow1, void* ws, size_t ws_bytes, void* stream);
 
+/* K2t -- the eigenpairs with lambda >= floor_rel * lambda_max of a symmetric positive
+ * semidefinite n x n H by Householder tridiagonalisation (one cooperative launch + one DMMA GEMM
+ * per 64-column panel), relative-accuracy Sturm multisection and one twisted factorisation per
+ * eigenvalue on a single definite representation T - sigma I = L D L^T (no re-orthogonalisation),
+ * and a compact-WY back-transformation.  Replaces scipy.linalg.eigh (pod.py:329-331) for the
+ * large preconditioned eigenproblems H = L^T L of a node POD: ~4/3 n^3 flops + 8 n^3 / 3 bytes of
+ * matrix reads instead of the block Jacobi's ~90 n^3 flops.  lam_desc (n, device): the K
+ * eigenvalues descending, the rest zero; W (n x n, ldw even): eigenvectors in the first K columns.
+ * status (host): 0 = done; 1 = declined -- the spectrum has a relative gap below relgap_min (the
+ * eigenvectors of a cluster would not be orthogonal) or no definite representation exists -- and
+ * the caller uses hp_syev instead; outputs are then not meaningful.  diag4 (nullable, host):
+ * {smallest relative gap, largest relative residual, sigma, K}.  2 <= n <= hp_syev_tri_max_order(). */
+int64_t hp_syev_tri_max_order(void);
+size_t hp_syev_tri_workspace_bytes(int64_t n);
+int hp_syev_tri(const double* H, int64_t ldh, int64_t n, double floor_rel, double relgap_min, double* lam_desc,
+                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag4, void* ws, size_t ws_bytes,
+                void* stream);
+
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):
  * keep = lam >= cutoff*lam_max*m, sigma = sqrt(lam_keep), N = smallest rank
  * whose tail sum_{n>=N} sigma_n^2 <= eps^2, tail = sum lam_keep[N:].

@@ -51,6 +51,10 @@ _SIGNATURES = {
     "hp_syev_padded_order": (c_i64, [c_i64]),
     "hp_syev_rows": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int,
                              ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), c_i64, c_i64, c_vp, c_size, c_vp]),
+    "hp_syev_tri_max_order": (c_i64, []),
+    "hp_syev_tri_workspace_bytes": (c_size, [c_i64]),
+    "hp_syev_tri": (c_int, [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64),
+                            ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), c_vp, c_size, c_vp]),
     "hp_truncate": (c_int, [c_vp, c_i64, c_dbl, c_dbl, c_i64, c_vp, c_vp, c_vp]),
     "hp_assemble_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "hp_assemble": (c_int, [VecSet, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_size, c_vp]),

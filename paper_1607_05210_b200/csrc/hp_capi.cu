@@ -43,6 +43,11 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
              double tol_rel, double tol_abs, double tol_angle, double keep_floor, int max_sweeps, int refine,
              int* sweeps_out, double* flops_out, void* ws, size_t ws_bytes, cudaStream_t st, int64_t vrow0 = 0,
              int64_t vrow1 = -1);
+int64_t syev_tri_max_order();
+size_t syev_tri_workspace_bytes(int64_t n);
+int syev_tri_run(const double* H, int64_t ldh, int64_t n, double floor_rel, double relgap_min, double* lam_desc,
+                 double* W, int64_t ldw, int64_t* k_out, int* status_out, double* diag, void* ws, size_t ws_bytes,
+                 cudaStream_t st);
 int truncate_run(const double* lam, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info,
                  cudaStream_t st);
 int drift_run(const double* C, int64_t ldc, int64_t n, double* out, cudaStream_t st);
@@ -243,6 +248,19 @@ int hp_syev_rows(const double* G, int64_t ldg, int64_t n, double* lam_desc, doub
                  double* flops, int64_t vrow0, int64_t vrow1, void* ws, size_t ws_bytes, void* stream) {
   return syev_run(G, ldg, n, lam_desc, V, ldv, nvec, tol_rel, tol_abs, tol_angle, keep_floor, max_sweeps, 0, sweeps,
                   flops, ws, ws_bytes, (cudaStream_t)stream, vrow0, vrow1);
+}
+
+int64_t hp_syev_tri_max_order(void) { return syev_tri_max_order(); }
+
+size_t hp_syev_tri_workspace_bytes(int64_t n) { return syev_tri_workspace_bytes(n); }
+
+int hp_syev_tri(const double* H, int64_t ldh, int64_t n, double floor_rel, double relgap_min, double* lam_desc,
+                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag4, void* ws, size_t ws_bytes,
+                void* stream) {
+  HP_REQUIRE(H && lam_desc && W && k_out && status && ws, "hp_syev_tri: null argument");
+  HP_REQUIRE(floor_rel >= 0.0 && relgap_min >= 0.0, "hp_syev_tri: negative threshold");
+  return syev_tri_run(H, ldh, n, floor_rel, relgap_min, lam_desc, W, ldw, k_out, status, diag4, ws, ws_bytes,
+                      (cudaStream_t)stream);
 }
 
 int hp_truncate(const double* lam_desc, int64_t n, double eps, double cutoff, int64_t m, double* sigma, double* info4,

@@ -301,3 +301,81 @@ def test_syev_rows_partition_is_bitwise_the_full_solve(n, cuts):
         merged[a:min(b, n)] = v_p[a:min(b, n)]
     assert np.array_equal(merged, v_full)
     assert np.max(np.abs(v_full.T @ v_full - np.eye(n))) < 1e-12 * np.sqrt(n)
+
+
+def _tri_solve(g, floor_rel, relgap_min=1e-9):
+    n = g.shape[0]
+    G = D.upload(g)
+    lam_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    W = D.DevMat.empty(n, n)
+    w = ws(lib.hp_syev_tri_workspace_bytes(n))
+    k = ctypes.c_int64(0)
+    status = ctypes.c_int(1)
+    diag = (ctypes.c_double * 4)()
+    N.check(lib.hp_syev_tri(G.ptr, G.ld, n, floor_rel, relgap_min, lam_d.data_ptr(), W.ptr, W.ld, ctypes.byref(k),
+                            ctypes.byref(status), diag, w.data_ptr(), w.numel(), st()), "syev_tri")
+    torch.cuda.synchronize()
+    return status.value, int(k.value), lam_d.cpu().numpy(), W.to_numpy(), list(diag)
+
+
+@pytest.mark.parametrize("n,decades", [(2, 1), (3, 2), (65, 3), (130, 6), (517, 10), (1024, 12), (1500, 13)])
+def test_syev_tri_graded_spectrum_vs_eigh(n, decades):
+    """hp_syev_tri (tridiagonalisation + relative multisection + twisted factorisation, no
+    re-orthogonalisation) on graded positive definite matrices -- the preconditioned Gramians
+    H = L^T L of a node POD (eigh at pod.py:329): eigenvalues to u * lambda_max, numerically
+    orthogonal eigenvectors, small residuals; odd / even orders, partial last panels."""
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = 10.0 ** (-decades * np.arange(n) / max(n - 1, 1))
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    floor_rel = 10.0 ** (-decades - 0.5)
+    status, k, ev, w, diag = _tri_solve(g, floor_rel)
+    ref = np.linalg.eigvalsh(g)[::-1]
+    print(f"syev_tri n={n}: status {status} K {k} min relgap {diag[0]:.2e} max resid {diag[1]:.2e}")
+    assert status == 0
+    assert k == int((ref >= floor_rel * ref[0]).sum()) == n
+    assert np.max(np.abs(ev[:k] - ref[:k])) <= 64 * 2.0 ** -52 * ref[0] * max(1.0, np.sqrt(n) / 8)
+    assert np.all(ev[k:] == 0.0)
+    wk = w[:, :k]
+    orth = np.max(np.abs(wk.T @ wk - np.eye(k)))
+    res = np.max(np.abs(g @ wk - wk * ev[None, :k])) / ref[0]
+    print(f"   |ev - ref| / lam_max {np.max(np.abs(ev[:k] - ref[:k])) / ref[0]:.2e} orth {orth:.2e} resid {res:.2e}")
+    assert orth <= 1e-10
+    assert res <= 1e-13 * max(1.0, np.sqrt(n) / 4)
+
+
+def test_syev_tri_floor_selects_leading_pairs():
+    rng = np.random.default_rng(7)
+    n = 700
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = 10.0 ** (-15 * np.arange(n) / (n - 1))
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    status, k, ev, w, diag = _tri_solve(g, 1e-9)
+    ref = np.linalg.eigvalsh(g)[::-1]
+    assert status == 0
+    kref = int((ref >= 1e-9 * ref[0]).sum())
+    assert abs(k - kref) <= 1
+    assert np.max(np.abs(ev[:k] - ref[:k])) <= 1e-13 * ref[0]
+    wk = w[:, :k]
+    assert np.max(np.abs(wk.T @ wk - np.eye(k))) <= 1e-10
+    # the computed vectors span the leading invariant subspace
+    vref = np.linalg.eigh(g)[1][:, ::-1][:, : k - 5]
+    assert np.linalg.norm(vref - wk @ (wk.T @ vref), 2) <= 1e-6
+
+
+def test_syev_tri_declines_clusters():
+    """A spectrum with (numerically) multiple eigenvalues cannot be resolved without
+    re-orthogonalisation: the solver must decline (status 1) so that the caller runs hp_syev."""
+    n = 300
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([np.full(n // 2, 2.0), np.full(n - n // 2, 1.0)])
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    status, k, ev, w, diag = _tri_solve(g, 1e-12)
+    print("clustered: status", status, "min relgap", diag[0])
+    assert status == 1
+    status, *_ = _tri_solve(np.eye(n), 1e-12)
+    assert status == 1
