@@ -23,7 +23,7 @@ const char* last_error() { return g_last_error.c_str(); }
 
 char* pinned_scratch() {
   thread_local char* buf = nullptr;
-  if (!buf && cudaMallocHost(&buf, 256) != cudaSuccess) buf = nullptr;
+  if (!buf && cudaMallocHost(&buf, 512) != cudaSuccess) buf = nullptr;
   return buf;
 }
 

@@ -134,7 +134,7 @@ int num_sms();
 
 // Diagnostics switched on through the C-ABI (hp_set_debug), never through the environment:
 // they only add CUDA-event timing printouts and never change a result.
-enum DebugFlags { DBG_JACOBI_TRACE = 1, DBG_JACOBI_ROUND_TIMING = 2, DBG_CHOL_TRACE = 4 };
+enum DebugFlags { DBG_JACOBI_TRACE = 1, DBG_JACOBI_ROUND_TIMING = 2, DBG_CHOL_TRACE = 4, DBG_TRI_TRACE = 8 };
 int debug_flags();
 
 // One-time per-DEVICE setup of kernel attributes (cudaFuncSetAttribute applies to the current
@@ -155,7 +155,8 @@ int once_per_device(std::atomic<unsigned long long>& mask, F&& setup) {
 }
 // Pinned host scratch of the calling host thread (allocated once, never freed per call: a
 // cudaFreeHost per call would synchronise the whole device and serialise concurrent node
-// streams).  Slots: [0, 64) Jacobi sweep counters, [64, 128) re-orthonormalisation flags.
+// streams).  512 bytes; slots: [0, 64) Jacobi sweep counters, [64, 128) re-orthonormalisation flags,
+// [128, 160) pivoted Cholesky, [256, 384) tridiagonal eigensolver.
 char* pinned_scratch();
 
 

@@ -339,13 +339,26 @@ __global__ void max_diag_kernel(const double* d, int64_t m, double* out) {
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
-// y = G x (G symmetric, column-major): one thread per row, coalesced over columns
-__global__ void gemv_sym(const double* G, int64_t ldg, int64_t m, const double* x, double* y) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double s = 0.0;
-  for (int64_t j = 0; j < m; ++j) s += G[j * ldg + i] * x[j];
-  y[i] = s;
+// y = G x (G symmetric, column-major): y_j = G[:, j] . x, one warp per column (contiguous reads,
+// four independent partial sums per lane, fixed-order combination)
+__global__ void __launch_bounds__(256) gemv_sym(const double* __restrict__ G, int64_t ldg, int64_t m,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= m) return;
+  const double* g = G + j * ldg;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t i = lane;
+  for (; i + 96 < m; i += 128) {
+    s0 = fma(g[i], x[i], s0);
+    s1 = fma(g[i + 32], x[i + 32], s1);
+    s2 = fma(g[i + 64], x[i + 64], s2);
+    s3 = fma(g[i + 96], x[i + 96], s3);
+  }
+  for (; i < m; i += 32) s0 = fma(g[i], x[i], s0);
+  double s = (s0 + s1) + (s2 + s3);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[j] = s;
 }
 
 // x = y / ||y||, out = ||y|| (single CTA, fixed-order reduction)
@@ -434,7 +447,7 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
     fill_value<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(px, m, 1.0 / sqrt((double)m));
     HP_CHECK_LAUNCH("fill_value");
     for (int it = 0; it < 8; ++it) {
-      gemv_sym<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, m, px, py);
+      gemv_sym<<<(unsigned)ceil_div(m * 32, 256), 256, 0, st>>>(A, lda, m, px, py);
       HP_CHECK_LAUNCH("gemv_sym");
       normalise<<<1, 256, 0, st>>>(py, m, px, lam_est);
       HP_CHECK_LAUNCH("normalise");

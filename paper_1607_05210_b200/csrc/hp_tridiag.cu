@@ -5,15 +5,16 @@
 // fixed reduction orders):
 //
 //   1. sytrd_panel  : H = Q T Q^T.  One cooperative launch per 64-column panel; a column step is
-//                     three grid-wide phases -- (P1) the deferred rank-2 corrections give the
-//                     current column x, (P2) every column dot A[:, c] . x of the trailing matrix
-//                     (HBM/L2-bound: the matrix is symmetric, so the matrix-vector product is a
-//                     set of contiguous column dots, each owned by one CTA -- no cross-CTA
-//                     partial sums), together with the panel dots V^T x, W^T x, (P3) the
-//                     Householder scalars, v, and w = tau (A v - V W^T v - W V^T v).  The
-//                     reflector is applied unscaled (v = s x + t e_1), so its norm needs no
-//                     phase of its own.  The trailing update A -= V W^T + W V^T is one DMMA
-//                     GEMM per panel ([V|W] [W|V]^T, exactly symmetric output).
+//                     two grid-wide phases -- (P2) every column dot A[:, c] . x of the trailing
+//                     matrix with the current column x (HBM/L2-bound: the matrix is symmetric, so
+//                     the matrix-vector product is a set of contiguous column dots, each owned by
+//                     one CTA -- no cross-CTA partial sums), together with the panel dots V^T x,
+//                     W^T x and x^T A x; (P3) the Householder scalars, v, w = tau (A v - V W^T v
+//                     - W V^T v) + alpha' v and the NEXT column x in one pass over the panel rows.
+//                     The reflector is applied unscaled (v = s x + t e_1) and w^T v is obtained
+//                     from v^T A v - 2 (V^T v).(W^T v), so neither the norm nor alpha' needs a
+//                     grid-wide phase of its own.  The trailing update A -= V W^T + W V^T is one
+//                     DMMA GEMM per panel ([V|W] [W|V]^T, exactly symmetric output).
 //   2. tri_*        : eigenvalues >= floor and their eigenvectors of T without any
 //                     re-orthogonalisation (MRRR with a single root representation): T - sigma I
 //                     = L D L^T with sigma just below lambda_min, so every eigenvalue is defined
@@ -29,6 +30,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 
 #include "hp_common.cuh"
 
@@ -44,6 +46,7 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_uppe
 namespace trd {
 
 constexpr int NB = 64;    // panel width
+constexpr int BT = 256;   // reflectors per compact-WY block of the back-transformation
 constexpr int TT = 512;   // threads per CTA of the panel kernel
 constexpr int NW = TT / 32;
 constexpr unsigned FULL = 0xffffffffu;
@@ -60,7 +63,6 @@ struct Panel {
   int64_t ldv;
   double* x;
   double* y;
-  double* wt;
   double* pxv;
   double* pxw;
   double* red;
@@ -69,6 +71,7 @@ struct Panel {
   double* tau;
   int j0, j1;
   int per_max;
+  unsigned long long* prof;  // optional phase timing (8 size buckets x 6 phases, ns), CTA 0 thread 0
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -93,6 +96,18 @@ __device__ __forceinline__ double block_sum(double v, double* buf) {
   return r;
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// w_r = tau (A v - V W^T v - W V^T v)_r + alpha' v_r: one expression shared by the row owners and by
+// the CTA-local copy of row j+1, so both produce the same bits
+__device__ __forceinline__ double w_entry(double tau, double av, double acc, double alpha_p, double v) {
+  return fma(alpha_p, v, tau * (av - acc));
+}
+
 __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -108,72 +123,30 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
   double* part = rbuf + 32;  // NW * per_max
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, cta = blockIdx.x;
-  const int sub = lane & 3;
-  const int wbase = ((cta * TT + tid) >> 5) * 8;  // first row group of this warp (8 groups of 4 lanes)
-  const int wstride = (G * TT) >> 2;
+  const int sub8 = lane & 7;
+  const int wbase8 = ((cta * TT + tid) >> 5) * 4;  // first row of this warp (4 rows of 8 lanes)
+  const int wstride8 = (G * TT) >> 3;
   const int64_t ldp = p.ldp;
   double* Pv = p.P;
   double* Pw = p.P + (int64_t)NB * ldp;
   double* Qw = p.Q;
   double* Qv = p.Q + (int64_t)NB * ldp;
-  double tau_prev = 0.0;
+  const bool prof = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
 
-  for (int j = p.j0; j <= p.j1; ++j) {
+  // the panel's first column: the trailing matrix is fully updated
+  for (int r = p.j0 + cta * TT + tid; r < n; r += G * TT) {
+    const double a = p.A[r + (int64_t)p.j0 * p.lda];
+    if (r == p.j0)
+      p.d[r] = a;
+    else
+      p.x[r] = a;
+  }
+  grid.sync();
+
+  for (int j = p.j0; j < p.j1; ++j) {
     const int i = j - p.j0;
-    // ------------------------------------------------------------------ P1: finish w_{i-1}, column x
-    double alpha_p = 0.0;
-    if (i > 0) {
-      if (warp == 0) {
-        double s = 0.0;
-        for (int c = lane; c < G; c += 32) s += __ldcg(p.red + c);
-        s = warp_sum(s);
-        if (lane == 0) scal[5] = -0.5 * tau_prev * s;
-      }
-      __syncthreads();
-      alpha_p = scal[5];
-    }
-    const bool stop_here = (j == p.j1) && (p.j1 < n - 1);  // panel end: only finish the last w
-    if (tid < i) {
-      const double vv = __ldcg(Pv + j + (int64_t)tid * ldp);
-      double wv;
-      if (tid == i - 1)
-        wv = __ldcg(p.wt + j) + alpha_p * vv;
-      else
-        wv = __ldcg(Pw + j + (int64_t)tid * ldp);
-      rowV[tid] = vv;
-      rowW[tid] = wv;
-    }
-    __syncthreads();
-    for (int rb = j + wbase; rb < n; rb += wstride) {
-      const int r = rb + (lane >> 2);
-      const bool valid = r < n;
-      double acc = 0.0, wfin = 0.0;
-      const bool fin = valid && i > 0 && sub == ((i - 1) & 3);
-      if (fin) wfin = __ldcg(p.wt + r) + alpha_p * __ldcg(Pv + r + (int64_t)(i - 1) * ldp);
-      if (valid && !stop_here) {
-        for (int c = sub; c < i; c += 4) {
-          const double vv = __ldcg(Pv + r + (int64_t)c * ldp);
-          const double ww = (c == i - 1) ? wfin : __ldcg(Pw + r + (int64_t)c * ldp);
-          acc = fma(vv, rowW[c], acc);
-          acc = fma(ww, rowV[c], acc);
-        }
-      }
-      if (fin) {
-        Pw[r + (int64_t)(i - 1) * ldp] = wfin;
-        Qw[r + (int64_t)(i - 1) * ldp] = wfin;
-      }
-      acc += __shfl_xor_sync(FULL, acc, 1);
-      acc += __shfl_xor_sync(FULL, acc, 2);
-      if (valid && !stop_here && sub == 0) {
-        const double a = p.A[r + (int64_t)j * p.lda] - acc;
-        if (r == j)
-          p.d[j] = a;
-        else
-          p.x[r] = a;
-      }
-    }
-    if (j == p.j1) break;
-    grid.sync();
+    unsigned long long tp[4];
+    if (prof) tp[0] = gtime();
     // ------------------------------------------------------------------ P2: column dots with x
     const int r0 = (j + 1) & ~1;
     const int len = nev - r0;
@@ -205,55 +178,101 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
           ptr = Pw + (int64_t)(tk - nr - i) * ldp + r0;
         return reinterpret_cast<const double2*>(ptr);
       };
-      for (int tb = t0; tb < t1; tb += 4) {
-        const double2* q0 = task_ptr(tb);
-        const double2* q1 = task_ptr(tb + 1);
-        const double2* q2 = task_ptr(tb + 2);
-        const double2* q3 = task_ptr(tb + 3);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 2
-        for (int q = tid; q < len2; q += TT) {
-          const double2 xv = xs2[q];
-          const double2 v0 = __ldcg(q0 + q);
-          const double2 v1 = __ldcg(q1 + q);
-          const double2 v2 = __ldcg(q2 + q);
-          const double2 v3 = __ldcg(q3 + q);
-          a0 = fma(v0.x, xv.x, a0);
-          a0 = fma(v0.y, xv.y, a0);
-          a1 = fma(v1.x, xv.x, a1);
-          a1 = fma(v1.y, xv.y, a1);
-          a2 = fma(v2.x, xv.x, a2);
-          a2 = fma(v2.y, xv.y, a2);
-          a3 = fma(v3.x, xv.x, a3);
-          a3 = fma(v3.y, xv.y, a3);
+      const bool wmode = per <= NW;  // few short columns: one warp per column, no cross-warp sums
+      if (wmode) {
+        if (t0 + warp < t1) {
+          const double2* q0 = task_ptr(t0 + warp);
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int q = lane;
+          for (; q + 96 < len2; q += 128) {
+            const double2 v0 = __ldcg(q0 + q), v1 = __ldcg(q0 + q + 32), v2 = __ldcg(q0 + q + 64),
+                          v3 = __ldcg(q0 + q + 96);
+            const double2 x0 = xs2[q], x1 = xs2[q + 32], x2 = xs2[q + 64], x3 = xs2[q + 96];
+            a0 = fma(v0.x, x0.x, a0);
+            a0 = fma(v0.y, x0.y, a0);
+            a1 = fma(v1.x, x1.x, a1);
+            a1 = fma(v1.y, x1.y, a1);
+            a2 = fma(v2.x, x2.x, a2);
+            a2 = fma(v2.y, x2.y, a2);
+            a3 = fma(v3.x, x3.x, a3);
+            a3 = fma(v3.y, x3.y, a3);
+          }
+          for (; q < len2; q += 32) {
+            const double2 v0 = __ldcg(q0 + q);
+            const double2 x0 = xs2[q];
+            a0 = fma(v0.x, x0.x, a0);
+            a0 = fma(v0.y, x0.y, a0);
+          }
+          a0 = warp_sum((a0 + a1) + (a2 + a3));
+          if (lane == 0) part[warp] = a0;
         }
-        a0 = warp_sum(a0);
-        a1 = warp_sum(a1);
-        a2 = warp_sum(a2);
-        a3 = warp_sum(a3);
-        if (lane == 0) {
-          double* dst = part + warp * p.per_max + (tb - t0);
-          dst[0] = a0;
-          if (tb + 1 < t1) dst[1] = a1;
-          if (tb + 2 < t1) dst[2] = a2;
-          if (tb + 3 < t1) dst[3] = a3;
+      } else {
+        // serpentine: odd columns walk their chunk backwards, so a sweep starts on the part of the
+        // trailing matrix the previous sweep left in L2
+        const int ngroup = (t1 - t0 + 3) >> 2;
+        for (int g = 0; g < ngroup; ++g) {
+          const int tb = t0 + 4 * ((j & 1) ? ngroup - 1 - g : g);
+          const double2* q0 = task_ptr(tb);
+          const double2* q1 = task_ptr(tb + 1);
+          const double2* q2 = task_ptr(tb + 2);
+          const double2* q3 = task_ptr(tb + 3);
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 2
+          for (int q = tid; q < len2; q += TT) {
+            const double2 xv = xs2[q];
+            const double2 v0 = __ldcg(q0 + q);
+            const double2 v1 = __ldcg(q1 + q);
+            const double2 v2 = __ldcg(q2 + q);
+            const double2 v3 = __ldcg(q3 + q);
+            a0 = fma(v0.x, xv.x, a0);
+            a0 = fma(v0.y, xv.y, a0);
+            a1 = fma(v1.x, xv.x, a1);
+            a1 = fma(v1.y, xv.y, a1);
+            a2 = fma(v2.x, xv.x, a2);
+            a2 = fma(v2.y, xv.y, a2);
+            a3 = fma(v3.x, xv.x, a3);
+            a3 = fma(v3.y, xv.y, a3);
+          }
+          a0 = warp_sum(a0);
+          a1 = warp_sum(a1);
+          a2 = warp_sum(a2);
+          a3 = warp_sum(a3);
+          if (lane == 0) {
+            double* dst = part + warp * p.per_max + (tb - t0);
+            dst[0] = a0;
+            if (tb + 1 < t1) dst[1] = a1;
+            if (tb + 2 < t1) dst[2] = a2;
+            if (tb + 3 < t1) dst[3] = a3;
+          }
         }
       }
       __syncthreads();
+      double xa = 0.0;  // this CTA's share of x^T A x
       for (int k = tid; k < t1 - t0; k += TT) {
-        double s = 0.0;
-        for (int w = 0; w < NW; ++w) s += part[w * p.per_max + k];
+        double s;
+        if (wmode) {
+          s = part[k];
+        } else {
+          s = 0.0;
+          for (int w = 0; w < NW; ++w) s += part[w * p.per_max + k];
+        }
         const int tk = t0 + k;
-        if (tk < nr)
+        if (tk < nr) {
           p.y[j + 1 + tk] = s;
-        else if (tk < nr + i)
+          xa = fma(s, xs[j + 1 + tk - r0], xa);
+        } else if (tk < nr + i) {
           p.pxv[tk - nr] = s;
-        else
+        } else {
           p.pxw[tk - nr - i] = s;
+        }
       }
+      xa = block_sum(xa, rbuf);
+      if (tid == 0) p.red[cta] = xa;
     }
+    if (prof) tp[1] = gtime();
     grid.sync();
-    // ------------------------------------------------------------------ P3: reflector, w
+    if (prof) tp[2] = gtime();
+    // ------------------------------------------------------------------ P3: reflector, w, next column
     double tau, beta, s, t;
     {
       const double xnorm = sqrt(ssq);
@@ -274,38 +293,101 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
       p.tau[j] = tau;
     }
     if (tid < i) {
-      cV[tid] = s * __ldcg(p.pxv + tid) + t * __ldcg(Pv + (j + 1) + (int64_t)tid * ldp);
-      cW[tid] = s * __ldcg(p.pxw + tid) + t * __ldcg(Pw + (j + 1) + (int64_t)tid * ldp);
+      const double rv = __ldcg(Pv + (j + 1) + (int64_t)tid * ldp);
+      const double rw = __ldcg(Pw + (j + 1) + (int64_t)tid * ldp);
+      rowV[tid] = rv;
+      rowW[tid] = rw;
+      cV[tid] = s * __ldcg(p.pxv + tid) + t * rv;
+      cW[tid] = s * __ldcg(p.pxw + tid) + t * rw;
+    } else if (tid < NB) {
+      rowV[tid] = rowW[tid] = cV[tid] = cW[tid] = 0.0;
     }
     __syncthreads();
-    double pwv = 0.0;
-    for (int rb = j + 1 + wbase; rb < n; rb += wstride) {
-      const int r = rb + (lane >> 2);
+    if (warp == 0) {  // x^T A x: the CTA partials in a fixed order
+      double a = 0.0;
+      for (int c = lane; c < G; c += 32) a += __ldcg(p.red + c);
+      a = warp_sum(a);
+      if (lane == 0) scal[0] = a;
+    } else if (warp == 1) {  // (V^T v) . (W^T v)
+      double a = 0.0;
+      for (int c = lane; c < i; c += 32) a = fma(cV[c], cW[c], a);
+      a = warp_sum(a);
+      if (lane == 0) scal[1] = a;
+    } else if (warp == 2) {  // row j+1 of V W^T v + W V^T v, in the row owner's summation order
+      double a = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = sub8 + 8 * u;
+        a = fma(rowV[c], cW[c], a);
+        a = fma(rowW[c], cV[c], a);
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) a += __shfl_xor_sync(FULL, a, o);
+      if (lane == 0) scal[2] = a;
+    }
+    __syncthreads();
+    // w^T v = tau (v^T A v - 2 (V^T v).(W^T v)) with v = s x + t e_1: no grid-wide reduction of its own
+    const double y1 = __ldcg(p.y + j + 1);
+    const double a11 = p.A[(j + 1) + (int64_t)(j + 1) * p.lda];
+    const double vAv = s * s * scal[0] + 2.0 * s * t * y1 + t * t * a11;
+    const double alpha_p = -0.5 * tau * (tau * (vAv - 2.0 * scal[1]));
+    const double vj1 = (tau == 0.0) ? 0.0 : 1.0;
+    const double wrow = w_entry(tau, s * y1 + t * a11, scal[2], alpha_p, vj1);  // W[j+1, i]
+    const bool do_next = (j + 1 < p.j1) || (p.j1 == n - 1);
+    for (int rb = j + 1 + wbase8; rb < n; rb += wstride8) {  // 8 lanes per row, every panel load in flight at once
+      const int r = rb + (lane >> 3);
       const bool valid = r < n;
-      double acc = 0.0;
-      if (valid) {
-        for (int c = sub; c < i; c += 4) {
-          acc = fma(__ldcg(Pv + r + (int64_t)c * ldp), cW[c], acc);
-          acc = fma(__ldcg(Pw + r + (int64_t)c * ldp), cV[c], acc);
+      double acc1 = 0.0, acc2 = 0.0;
+      {
+        double vv[8], ww[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = sub8 + 8 * u;
+          const bool on = valid && c < i;
+          vv[u] = on ? __ldcg(Pv + r + (int64_t)c * ldp) : 0.0;
+          ww[u] = on ? __ldcg(Pw + r + (int64_t)c * ldp) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = sub8 + 8 * u;  // c < NB: the coefficient arrays are zero past i
+          acc1 = fma(vv[u], cW[c], acc1);
+          acc1 = fma(ww[u], cV[c], acc1);
+          acc2 = fma(vv[u], rowW[c], acc2);
+          acc2 = fma(ww[u], rowV[c], acc2);
         }
       }
-      acc += __shfl_xor_sync(FULL, acc, 1);
-      acc += __shfl_xor_sync(FULL, acc, 2);
-      if (valid && sub == 0) {
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        acc1 += __shfl_xor_sync(FULL, acc1, o);
+        acc2 += __shfl_xor_sync(FULL, acc2, o);
+      }
+      if (valid && sub8 == 0) {
         const double v = (tau == 0.0) ? 0.0 : ((r == j + 1) ? 1.0 : s * xs[r - r0]);
-        const double av = s * __ldcg(p.y + r) + t * p.A[r + (int64_t)(j + 1) * p.lda];
-        const double wtil = tau * (av - acc);
+        const double anext = p.A[r + (int64_t)(j + 1) * p.lda];
+        const double w = w_entry(tau, s * __ldcg(p.y + r) + t * anext, acc1, alpha_p, v);
         Pv[r + (int64_t)i * ldp] = v;
         Qv[r + (int64_t)i * ldp] = v;
         p.Vall[r + (int64_t)j * p.ldv] = v;
-        p.wt[r] = wtil;
-        pwv = fma(wtil, v, pwv);
+        Pw[r + (int64_t)i * ldp] = w;
+        Qw[r + (int64_t)i * ldp] = w;
+        if (do_next) {
+          const double xn = anext - acc2 - (v * wrow + w * vj1);
+          if (r == j + 1)
+            p.d[j + 1] = xn;
+          else
+            p.x[r] = xn;
+        }
       }
     }
-    const double tot = block_sum(pwv, rbuf);
-    if (tid == 0) p.red[cta] = tot;
-    tau_prev = tau;
+    if (prof) tp[3] = gtime();
     grid.sync();
+    if (prof) {
+      unsigned long long* b = p.prof + 6 * ((int)(((long long)j * 8) / n));
+      b[0] += tp[1] - tp[0];  // P2
+      b[1] += tp[2] - tp[1];  // sync B
+      b[2] += tp[3] - tp[2];  // P3
+      b[3] += gtime() - tp[3];  // sync A
+    }
   }
 }
 
@@ -346,19 +428,23 @@ __device__ bool ldl_factor(const double* a, const double* b, int n, double shift
   return ok;
 }
 
-enum { I_SIGMA = 0, I_LMAX, I_LMIN, I_K, I_OK, I_TNORM, I_PIVMIN, I_HI, I_LO, I_MINGAP, I_MAXRES, I_BAD, I_COUNT };
+enum { I_SIGMA = 0, I_LMAX, I_LMIN, I_K, I_OK, I_TNORM, I_PIVMIN, I_HI, I_LO, I_MINGAP, I_MAXRES, I_BAD, I_MAXIT, I_SUMIT, I_COUNT };
 
-// One CTA of 1024 threads: spectrum bounds, lambda_max / lambda_min by 1025-way multisection on a
-// safely definite representation, the count K of eigenvalues >= floor_rel * lambda_max, and the root
-// representation T - sigma I = L D L^T with sigma just below lambda_min.
-__global__ void __launch_bounds__(1024, 1) tri_prepare(const double* a, const double* b, int n, double floor_rel,
-                                                        double* d0, double* lld0, double* d1, double* l1, double* ld1,
-                                                        double* lld1, double* info) {
-  __shared__ double sh[40];
-  __shared__ double bounds[2];
+// One CTA of 512 threads (16 warps: the Sturm recurrences are division-latency chains, more warps
+// on the SM would only queue on its issue slots): spectrum bounds, lambda_max and lambda_min by
+// 257-way multisection on a safely definite representation (both at once, one half of the CTA
+// each), the count K of eigenvalues >= floor_rel * lambda_max, and the root representation
+// T - sigma I = L D L^T with sigma just below lambda_min.
+__global__ void __launch_bounds__(512, 1) tri_prepare(const double* a, const double* b, int n, double floor_rel,
+                                                       double* d0, double* lld0, double* d1, double* l1, double* ld1,
+                                                       double* lld1, double* info) {
+  __shared__ double sh[8];
+  __shared__ double bounds[2][2];
+  __shared__ int cnts[2];
+  __shared__ double red[4][16];
   const int tid = threadIdx.x;
   double gl = DBL_MAX, gu = -DBL_MAX, em = 0.0, tn = 0.0;
-  for (int i = tid; i < n; i += 1024) {
+  for (int i = tid; i < n; i += 512) {
     const double el = i > 0 ? fabs(b[i - 1]) : 0.0, er = i < n - 1 ? fabs(b[i]) : 0.0;
     gl = fmin(gl, a[i] - el - er);
     gu = fmax(gu, a[i] + el + er);
@@ -371,7 +457,6 @@ __global__ void __launch_bounds__(1024, 1) tri_prepare(const double* a, const do
     em = fmax(em, __shfl_xor_sync(FULL, em, o));
     tn = fmax(tn, __shfl_xor_sync(FULL, tn, o));
   }
-  __shared__ double red[4][32];
   if ((tid & 31) == 0) {
     red[0][tid >> 5] = gl;
     red[1][tid >> 5] = gu;
@@ -380,7 +465,7 @@ __global__ void __launch_bounds__(1024, 1) tri_prepare(const double* a, const do
   }
   __syncthreads();
   if (tid == 0) {
-    for (int w = 1; w < 32; ++w) {
+    for (int w = 1; w < 16; ++w) {
       gl = fmin(gl, red[0][w]);
       gu = fmax(gu, red[1][w]);
       em = fmax(em, red[2][w]);
@@ -393,36 +478,36 @@ __global__ void __launch_bounds__(1024, 1) tri_prepare(const double* a, const do
     sh[0] = sigma0;
     sh[1] = pivmin;
     sh[2] = tn;
-    sh[3] = (gu - sigma0) * (1.0 + 1e-10) + 16.0 * UNIT * tn;  // upper bound of the shifted spectrum
+    const double top = (gu - sigma0) * (1.0 + 1e-10) + 16.0 * UNIT * tn;  // bound of the shifted spectrum
+    bounds[0][0] = bounds[1][0] = 0.0;
+    bounds[0][1] = bounds[1][1] = top;
   }
   __syncthreads();
-  const double sigma0 = sh[0], pivmin = sh[1], tnorm = sh[2], top = sh[3];
-  double ext[2];
-  for (int which = 0; which < 2; ++which) {  // 0: lambda_max (ascending index n-1), 1: lambda_min (index 0)
-    const int want = which == 0 ? n - 1 : 0;
-    if (tid == 0) {
-      bounds[0] = 0.0;
-      bounds[1] = top;
-    }
+  const double sigma0 = sh[0], pivmin = sh[1], tnorm = sh[2];
+  const int which = tid >> 8;  // 0: lambda_max (ascending index n-1), 1: lambda_min (index 0)
+  const int want = which == 0 ? n - 1 : 0;
+  const int t = tid & 255;
+  for (int round = 0; round < 8; ++round) {
+    if (tid < 2) cnts[tid] = 0;
     __syncthreads();
-    for (int round = 0; round < 7; ++round) {
-      const double lo = bounds[0], hi = bounds[1];
-      const double step = (hi - lo) / 1025.0;
-      const double xq = lo + step * (double)(tid + 1);
-      const int c = negcount(d0, lld0, n, xq, pivmin);
-      const int cnt = __syncthreads_count(c <= want);  // points at or below the wanted eigenvalue
-      if (tid == 0) {
-        if (cnt > 0) bounds[0] = lo + step * (double)cnt;
-        if (cnt < 1024) bounds[1] = lo + step * (double)(cnt + 1);
-      }
-      __syncthreads();
+    const double lo = bounds[which][0], hi = bounds[which][1];
+    const double step = (hi - lo) / 257.0;
+    const double xq = lo + step * (double)(t + 1);
+    const int c = negcount(d0, lld0, n, xq, pivmin);
+    const unsigned okm = __ballot_sync(FULL, c <= want);  // points at or below the wanted eigenvalue
+    if ((tid & 31) == 0) atomicAdd(&cnts[which], __popc(okm));
+    __syncthreads();
+    if (t == 0) {
+      const int cnt = cnts[which];
+      if (cnt > 0) bounds[which][0] = lo + step * (double)cnt;
+      if (cnt < 256) bounds[which][1] = lo + step * (double)(cnt + 1);
     }
-    ext[which] = 0.5 * (bounds[0] + bounds[1]) + sigma0;
     __syncthreads();
   }
-  const double lam_max = ext[0], lam_min = ext[1];
-  const double floor_abs = floor_rel * lam_max;
   if (tid == 0) {
+    const double lam_max = 0.5 * (bounds[0][0] + bounds[0][1]) + sigma0;
+    const double lam_min = 0.5 * (bounds[1][0] + bounds[1][1]) + sigma0;
+    const double floor_abs = floor_rel * lam_max;
     int K = n;
     if (floor_abs - sigma0 > 0.0) K = n - negcount(d0, lld0, n, floor_abs - sigma0, pivmin);
     double delta = 256.0 * UNIT * tnorm;
@@ -445,8 +530,10 @@ __global__ void __launch_bounds__(1024, 1) tri_prepare(const double* a, const do
   }
 }
 
-// One warp per wanted eigenvalue (descending index k): 32-way multisection on a geometric grid, so
-// small eigenvalues are located to the same RELATIVE accuracy as large ones.
+// One warp per wanted eigenvalue (descending index k): 32-way multisection on a geometric grid (small
+// eigenvalues are located to the same RELATIVE accuracy as large ones) until the bracket holds
+// exactly this eigenvalue and is narrower than 2^-30 octaves; tri_getvec's Rayleigh-quotient
+// iteration converges in one step from there.  A cluster keeps subdividing (at most 14 rounds).
 __global__ void __launch_bounds__(256) tri_bisect(const double* d, const double* lld, int n, int K, const double* info,
                                                   double* lam_s, double* blo, double* bhi) {
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -455,47 +542,100 @@ __global__ void __launch_bounds__(256) tri_bisect(const double* d, const double*
   const int want = n - 1 - k;
   const double pivmin = info[I_PIVMIN];
   double lo = info[I_LO], hi = info[I_HI];
+  int clo = 0, chi = n;  // eigenvalues below lo / below hi
   for (int round = 0; round < 14; ++round) {
     const double lr = log2(hi / lo);
     if (!(lr > 8.0 * UNIT)) break;
+    if (clo == want && chi == want + 1 && lr <= 0x1p-30) break;
     double xq = lo * exp2(lr * (double)(lane + 1) / 33.0);
     xq = fmin(fmax(xq, lo), hi);
     const int c = negcount(d, lld, n, xq, pivmin);
     const unsigned okm = __ballot_sync(FULL, c <= want);
     const int cnt = __popc(okm);
     const double nlo = __shfl_sync(FULL, xq, max(cnt - 1, 0));
+    const int nclo = __shfl_sync(FULL, c, max(cnt - 1, 0));
     const double nhi = __shfl_sync(FULL, xq, min(cnt, 31));
-    if (cnt > 0) lo = nlo;
-    if (cnt < 32) hi = nhi;
+    const int nchi = __shfl_sync(FULL, c, min(cnt, 31));
+    if (cnt > 0) {
+      lo = nlo;
+      clo = nclo;
+    }
+    if (cnt < 32) {
+      hi = nhi;
+      chi = nchi;
+    }
   }
   if (lane == 0) {
     lam_s[k] = sqrt(lo) * sqrt(hi);
-    blo[k] = lo * (1.0 - 64.0 * UNIT);
-    bhi[k] = hi * (1.0 + 64.0 * UNIT);
+    blo[k] = lo;
+    bhi[k] = hi;
   }
+}
+
+// z_r = 1, z_i = -lplus_i z_{i+1} (i < r), z_{i+1} = -uminus_i z_i (i >= r): returns z^T z; with
+// STORE the entries are written scaled to column zc.  The factor loads run PF steps ahead of the
+// multiply chain (they depend on nothing but the index).
+constexpr int PF = 8;
+template <bool STORE>
+__device__ __forceinline__ double twisted_z(const double* __restrict__ lp, const double* __restrict__ um, int64_t kp,
+                                            int n, int r, double scale, double* __restrict__ zc) {
+  double ztz = 1.0, z = 1.0;
+  if (STORE) zc[r] = scale;
+  for (int i0 = r - 1; i0 >= 0; i0 -= PF) {
+    double f[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) f[u] = (i0 - u >= 0) ? lp[(int64_t)(i0 - u) * kp] : 0.0;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      if (i0 - u >= 0) {
+        z = -f[u] * z;
+        ztz = fma(z, z, ztz);
+        if (STORE) zc[i0 - u] = z * scale;
+      }
+    }
+  }
+  z = 1.0;
+  for (int i0 = r; i0 < n - 1; i0 += PF) {
+    double f[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) f[u] = (i0 + u < n - 1) ? um[(int64_t)(i0 + u) * kp] : 0.0;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      if (i0 + u < n - 1) {
+        z = -f[u] * z;
+        ztz = fma(z, z, ztz);
+        if (STORE) zc[i0 + u + 1] = z * scale;
+      }
+    }
+  }
+  return ztz;
 }
 
 // One thread per wanted eigenvalue: twisted factorisation (stationary qds from the top, progressive
 // qds from the bottom, twist where |gamma| is smallest), Rayleigh-quotient correction of the
-// eigenvalue (at most 3 passes), eigenvector written normalised to column k of Z.
+// eigenvalue inside the Sturm bracket (cubic convergence; a step that leaves the bracket becomes a
+// bisection), eigenvector written normalised to column k of Z.
 __global__ void __launch_bounds__(32) tri_getvec(const double* __restrict__ d, const double* __restrict__ l,
-                                                  const double* __restrict__ ld, const double* __restrict__ lld,
-                                                  int n, int K, int64_t kp, const double* info, double* lam_s,
-                                                  const double* blo, const double* bhi, double* __restrict__ LP,
-                                                  double* __restrict__ UM, double* __restrict__ PP,
-                                                  double* __restrict__ Z, int64_t ldz, double* lam_out,
-                                                  double* resid) {
+                                                 const double* __restrict__ ld, const double* __restrict__ lld,
+                                                 int n, int K, int64_t kp, const double* info, double* lam_s,
+                                                 const double* blo, const double* bhi, double* __restrict__ LP,
+                                                 double* __restrict__ UM, double* __restrict__ PP,
+                                                 double* __restrict__ Z, int64_t ldz, double* lam_out,
+                                                 double* resid, int* iters) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   const double pivmin = info[I_PIVMIN], sigma = info[I_SIGMA];
   double lam = lam_s[k];
-  const double lo = blo[k], hi = bhi[k];
+  double lo = blo[k], hi = bhi[k];
   double* lp = LP + k;
   double* um = UM + k;
   double* pp = PP + k;
   int r = 0;
   double gam = 0.0, ztz = 1.0;
-  for (int it = 0; it < 3; ++it) {
+  const int want = n - 1 - k;
+  constexpr int MAXIT = 5;
+  int its = 0;
+  for (int it = 0; it < MAXIT; ++it) {
     double pcur = d[n - 1] - lam;
     pp[(int64_t)(n - 1) * kp] = pcur;
     for (int i = n - 2; i >= 0; --i) {
@@ -507,84 +647,93 @@ __global__ void __launch_bounds__(32) tri_getvec(const double* __restrict__ d, c
       pp[(int64_t)i * kp] = pcur;
     }
     double s = -lam, sarr = 0.0;
-    gam = sarr + pp[0];
+    gam = sarr + pcur;  // pp[0]
     double best = fabs(gam);
     r = 0;
-    for (int i = 0; i < n - 1; ++i) {
-      double dp = d[i] + s;
-      if (fabs(dp) < pivmin) dp = -pivmin;
-      const double lpi = ld[i] / dp;
-      lp[(int64_t)i * kp] = lpi;
-      sarr = s * lpi * l[i];
-      s = sarr - lam;
-      const double g = sarr + pp[(int64_t)(i + 1) * kp];
-      if (fabs(g) < best) {
-        best = fabs(g);
-        gam = g;
-        r = i + 1;
+    int neg = 0;  // Sturm count at lam, a by-product of the stationary transform
+    for (int i0 = 0; i0 < n - 1; i0 += PF) {
+      double pb[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) pb[u] = (i0 + u < n - 1) ? pp[(int64_t)(i0 + u + 1) * kp] : 0.0;
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int i = i0 + u;
+        if (i < n - 1) {
+          double dp = d[i] + s;
+          if (fabs(dp) < pivmin) dp = -pivmin;
+          neg += dp < 0.0;
+          const double lpi = ld[i] / dp;
+          lp[(int64_t)i * kp] = lpi;
+          sarr = s * lpi * l[i];
+          s = sarr - lam;
+          const double g = sarr + pb[u];
+          if (fabs(g) < best) {
+            best = fabs(g);
+            gam = g;
+            r = i + 1;
+          }
+        }
       }
     }
-    ztz = 1.0;
-    double z = 1.0;
-    for (int i = r - 1; i >= 0; --i) {
-      z = -lp[(int64_t)i * kp] * z;
-      ztz = fma(z, z, ztz);
-    }
-    z = 1.0;
-    for (int i = r; i < n - 1; ++i) {
-      z = -um[(int64_t)i * kp] * z;
-      ztz = fma(z, z, ztz);
-    }
+    neg += (d[n - 1] + s) < 0.0;
+    ztz = twisted_z<false>(lp, um, kp, n, r, 1.0, nullptr);
     const double rq = gam / ztz;
-    if (it == 2 || !(fabs(rq) > 4.0 * UNIT * fabs(lam))) break;
-    const double nl = lam + rq;
-    if (!(nl > lo && nl < hi)) break;
+    if (neg <= want)
+      lo = fmax(lo, lam);
+    else
+      hi = fmin(hi, lam);
+    its = it + 1;
+    if (it == MAXIT - 1 || !(fabs(rq) > 8.0 * UNIT * fabs(lam))) break;
+    double nl = lam + rq;
+    // a step that leaves the bracket (beyond rounding slack) is replaced by a geometric bisection
+    if (!(nl > lo * (1.0 - 32.0 * UNIT) && nl < hi * (1.0 + 32.0 * UNIT))) nl = sqrt(lo) * sqrt(hi);
+    if (nl == lam) break;
     lam = nl;
   }
   const double scale = rsqrt(ztz);
-  double* zc = Z + (int64_t)k * ldz;
-  zc[r] = scale;
-  double z = 1.0;
-  for (int i = r - 1; i >= 0; --i) {
-    z = -lp[(int64_t)i * kp] * z;
-    zc[i] = z * scale;
-  }
-  z = 1.0;
-  for (int i = r; i < n - 1; ++i) {
-    z = -um[(int64_t)i * kp] * z;
-    zc[i + 1] = z * scale;
-  }
+  twisted_z<true>(lp, um, kp, n, r, scale, Z + (int64_t)k * ldz);
   lam_s[k] = lam;
   lam_out[k] = lam + sigma;
+  iters[k] = its;
   const double res = fabs(gam) * scale / fabs(lam);
   resid[k] = (isfinite(res) && isfinite(scale) && scale > 0.0) ? res : DBL_MAX;
 }
 
 // smallest relative gap between consecutive computed eigenvalues, largest relative residual
-__global__ void __launch_bounds__(1024, 1) tri_check(const double* lam_s, const double* resid, int K, int n,
-                                                     double* lam_out, double* info) {
-  __shared__ double r0[32], r1[32];
+__global__ void __launch_bounds__(1024, 1) tri_check(const double* lam_s, const double* resid, const int* iters, int K,
+                                                     int n, double* lam_out, double* info) {
+  __shared__ double r0[32], r1[32], r2[32], r3[32];
   const int tid = threadIdx.x;
-  double mg = DBL_MAX, mr = 0.0;
+  double mg = DBL_MAX, mr = 0.0, mi = 0.0, si = 0.0;
   for (int k = tid; k < K; k += 1024) {
     if (k + 1 < K) mg = fmin(mg, fabs(lam_s[k] - lam_s[k + 1]) / fabs(lam_s[k]));
     mr = fmax(mr, resid[k]);
+    mi = fmax(mi, (double)iters[k]);
+    si += (double)iters[k];
   }
   for (int k = K + tid; k < n; k += 1024) lam_out[k] = 0.0;
   for (int o = 16; o; o >>= 1) {
     mg = fmin(mg, __shfl_xor_sync(FULL, mg, o));
     mr = fmax(mr, __shfl_xor_sync(FULL, mr, o));
+    mi = fmax(mi, __shfl_xor_sync(FULL, mi, o));
+    si += __shfl_xor_sync(FULL, si, o);
   }
   if ((tid & 31) == 0) {
     r0[tid >> 5] = mg;
     r1[tid >> 5] = mr;
+    r2[tid >> 5] = mi;
+    r3[tid >> 5] = si;
   }
   __syncthreads();
   if (tid == 0) {
     for (int w = 1; w < 32; ++w) {
       mg = fmin(mg, r0[w]);
       mr = fmax(mr, r1[w]);
+      mi = fmax(mi, r2[w]);
+      si += r3[w];
     }
+    info[I_MAXIT] = mi;
+    info[I_SUMIT] = si;
     info[I_MINGAP] = mg;
     info[I_MAXRES] = mr;
     info[I_BAD] = (mr == DBL_MAX || !(mg == mg)) ? 1.0 : 0.0;
@@ -603,19 +752,34 @@ __global__ void tinv_build(double* S, int lds, const double* tau, int nb) {
     S[i + c * lds] = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
 }
 
-// Y <- T Y, i.e. solve the upper-triangular T^-1 Y' = Y; one thread per column of Y
+// Y <- T Y, i.e. solve the upper-triangular T^-1 Y' = Y (a diagonal block of at most NB rows); one
+// thread per column of Y with the column in registers (fully unrolled back-substitution, reciprocal
+// pivots from shared memory; rows past nb act as an identity block)
 __global__ void __launch_bounds__(128) trsm_tinv(const double* Tinv, int ldt, int nb, double* Y, int ldy, int K) {
   __shared__ double ts[NB * NB];
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) ts[e] = Tinv[(e % nb) + (e / nb) * ldt];
+  __shared__ double rd[NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int i = e % NB, c = e / NB;
+    ts[e] = (i < nb && c < nb && i < c) ? Tinv[i + (int64_t)c * ldt] : 0.0;
+  }
+  if (threadIdx.x < NB) rd[threadIdx.x] = threadIdx.x < nb ? 1.0 / Tinv[threadIdx.x + (int64_t)threadIdx.x * ldt] : 1.0;
   __syncthreads();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
-  double* y = Y + (int64_t)k * ldy;
-  for (int i = nb - 1; i >= 0; --i) {
+  double* yc = Y + (int64_t)k * ldy;
+  double y[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) y[i] = i < nb ? yc[i] : 0.0;
+#pragma unroll
+  for (int i = NB - 1; i >= 0; --i) {
     double s = y[i];
-    for (int c = i + 1; c < nb; ++c) s = fma(-ts[i + c * nb], y[c], s);
-    y[i] = s / ts[i + i * nb];
+#pragma unroll
+    for (int c = i + 1; c < NB; ++c) s = fma(-ts[i + c * NB], y[c], s);
+    y[i] = s * rd[i];
   }
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+    if (i < nb) yc[i] = y[i];
 }
 
 __global__ void copy_in(const double* H, int64_t ldh, int n, double* A, int64_t lda) {
@@ -641,11 +805,14 @@ size_t syev_tri_workspace_bytes(int64_t n) {
   o += 20 * al256((size_t)(n + 2) * 8);       // vectors
   o += 4 * al256(1024 * 8);                   // pxv, pxw, red, info
   o += 3 * al256((size_t)lda * n * 8);        // LP, UM, PP
-  o += al256((size_t)NB * n * 8) + al256((size_t)NB * NB * 8);  // Y, S
+  o += al256((size_t)BT * n * 8) + al256((size_t)BT * BT * 8);  // Y, S
   size_t g = gemm_workspace_bytes(n, n, 2 * NB, 1, 0);
-  g = std::max(g, gemm_workspace_bytes(NB, n, n, 0, 0));
-  g = std::max(g, gemm_workspace_bytes(n, n, NB, 0, 0));
-  g = std::max(g, gemm_workspace_bytes(NB, NB, n, 0, 0));
+  for (int64_t mb : {(int64_t)NB, (int64_t)(2 * NB), (int64_t)(3 * NB), (int64_t)BT}) {
+    g = std::max(g, gemm_workspace_bytes(mb, n, n, 0, 0));
+    g = std::max(g, gemm_workspace_bytes(n, n, mb, 0, 0));
+    g = std::max(g, gemm_workspace_bytes(mb, mb, n, 0, 0));
+    g = std::max(g, gemm_workspace_bytes(NB, n, mb, 0, 0));
+  }
   o += al256(g) + 256;
   return o;
 }
@@ -679,7 +846,7 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   double* Q = take((size_t)lda * 2 * NB * 8);
   double* vec[20];
   for (auto& v : vec) v = take((size_t)(n + 2) * 8);
-  double *x = vec[0], *y = vec[1], *wt = vec[2], *dT = vec[3], *eT = vec[4], *tau = vec[5], *d0 = vec[6],
+  double *x = vec[0], *y = vec[1], *dT = vec[3], *eT = vec[4], *tau = vec[5], *d0 = vec[6],
          *lld0 = vec[7], *d1 = vec[8], *l1 = vec[9], *ld1 = vec[10], *lld1 = vec[11], *lam_s = vec[12],
          *blo = vec[13], *bhi = vec[14], *resid = vec[15];
   double* pxv = take(1024 * 8);
@@ -689,11 +856,32 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   double* LP = take((size_t)lda * n * 8);
   double* UM = take((size_t)lda * n * 8);
   double* PP = take((size_t)lda * n * 8);
-  double* Y = take((size_t)NB * n * 8);
-  double* S = take((size_t)NB * NB * 8);
+  double* Y = take((size_t)BT * n * 8);
+  double* S = take((size_t)BT * BT * 8);
   void* gws = base + o;
   const size_t gwsb = ws_bytes - o;
 
+  // stage timing (hp_set_debug bit 3): CUDA events on the launching stream, printed at the end
+  const bool trace = (debug_flags() & DBG_TRI_TRACE) != 0;
+  cudaEvent_t ev[6] = {};
+  auto mark = [&](int i) {
+    if (trace && (ev[i] || cudaEventCreate(&ev[i]) == cudaSuccess)) cudaEventRecord(ev[i], st);
+  };
+  auto report = [&](int last) {
+    if (!trace) return;
+    cudaEventSynchronize(ev[last]);
+    static const char* names[] = {"sytrd", "prepare", "bisect+getvec", "check", "backtransform"};
+    fprintf(stderr, "[hp_syev_tri] n=%d", n);
+    for (int i = 0; i < last; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      fprintf(stderr, " %s=%.2fms", names[i], ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  mark(0);
   copy_in<<<(unsigned)ceil_div(lda * n, 256), 256, 0, st>>>(H, ldh, n, A, lda);
   HP_CHECK_LAUNCH("tri copy_in");
   HP_CHECK_CUDA(zero_async(Vall, (size_t)lda * n * 8, st));
@@ -701,12 +889,11 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   HP_CHECK_CUDA(zero_async(Q, (size_t)lda * 2 * NB * 8, st));
   HP_CHECK_CUDA(zero_async(x, (size_t)(n + 2) * 8, st));
   HP_CHECK_CUDA(zero_async(y, (size_t)(n + 2) * 8, st));
-  HP_CHECK_CUDA(zero_async(wt, (size_t)(n + 2) * 8, st));
-  count_launches(6);
+  count_launches(5);
 
   int nsm = num_sms();
   const int G = std::max(1, std::min(nsm, 1024));
-  const int per_max = (int)ceil_div((int64_t)n + 2 * NB, G) + 4;
+  const int per_max = std::max((int)ceil_div((int64_t)n + 2 * NB, G) + 4, NW);
   const int nev = (n + 1) & ~1;
   const size_t smem = (size_t)(nev + 2 + 4 * NB + 16 + 32 + (size_t)NW * per_max) * 8;
   HP_REQUIRE(smem <= 220 * 1024, "syev_tri: order too large for the panel kernel");
@@ -731,7 +918,6 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   p.ldv = lda;
   p.x = x;
   p.y = y;
-  p.wt = wt;
   p.pxv = pxv;
   p.pxw = pxw;
   p.red = red;
@@ -739,6 +925,11 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   p.e = eT;
   p.tau = tau;
   p.per_max = per_max;
+  p.prof = nullptr;
+  if (trace) {
+    p.prof = reinterpret_cast<unsigned long long*>(info + 512);
+    HP_CHECK_CUDA(zero_async(p.prof, 48 * 8, st));
+  }
   for (int j0 = 0; j0 < n - 1;) {
     const int j1 = std::min(j0 + NB, n - 1);
     p.j0 = j0;
@@ -758,12 +949,25 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
     j0 = j1;
   }
 
-  tri_prepare<<<1, 1024, 0, st>>>(dT, eT, n, floor_rel, d0, lld0, d1, l1, ld1, lld1, info);
+  mark(1);
+  if (trace) {
+    unsigned long long hp[48];
+    if (cudaMemcpyAsync(hp, p.prof, sizeof(hp), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+        cudaStreamSynchronize(st) == cudaSuccess) {
+      fprintf(stderr, "[sytrd_panel] per-phase ms by column octile (P2, syncB, P3, syncA)\n");
+      for (int b = 0; b < 8; ++b) {
+        fprintf(stderr, "  octile %d:", b);
+        for (int q = 0; q < 4; ++q) fprintf(stderr, " %7.2f", hp[6 * b + q] * 1e-6);
+        fprintf(stderr, "\n");
+      }
+    }
+  }
+  tri_prepare<<<1, 512, 0, st>>>(dT, eT, n, floor_rel, d0, lld0, d1, l1, ld1, lld1, info);
   HP_CHECK_LAUNCH("tri_prepare");
   char* pin = pinned_scratch();
   HP_REQUIRE(pin != nullptr, "syev_tri: pinned host scratch unavailable");
-  double* hinfo = reinterpret_cast<double*>(pin + 160);  // 12 doubles: [160, 256)
-  HP_CHECK_CUDA(d2h_small(hinfo, info, 12 * sizeof(double), st));
+  double* hinfo = reinterpret_cast<double*>(pin + 256);  // 16 doubles: [256, 384)
+  HP_CHECK_CUDA(d2h_small(hinfo, info, 16 * sizeof(double), st));
   count_launches(1);
   HP_CHECK_CUDA(cudaStreamSynchronize(st));
   const bool ok = hinfo[I_OK] != 0.0;
@@ -774,6 +978,8 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
     diag[2] = hinfo[I_SIGMA];
     diag[3] = (double)K;
   }
+  mark(2);
+  if (!ok || K <= 0) report(2);
   if (!ok) return HP_OK;  // declined
   if (K <= 0) {
     HP_CHECK_CUDA(zero_async(lam_desc, (size_t)n * 8, st));
@@ -784,43 +990,65 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   tri_bisect<<<(unsigned)ceil_div((int64_t)K * 32, 256), 256, 0, st>>>(d1, lld1, n, K, info, lam_s, blo, bhi);
   HP_CHECK_LAUNCH("tri_bisect");
   tri_getvec<<<(unsigned)ceil_div(K, 32), 32, 0, st>>>(d1, l1, ld1, lld1, n, K, lda, info, lam_s, blo, bhi, LP, UM,
-                                                         PP, W, ldw, lam_desc, resid);
+                                                         PP, W, ldw, lam_desc, resid, reinterpret_cast<int*>(vec[16]));
   HP_CHECK_LAUNCH("tri_getvec");
-  tri_check<<<1, 1024, 0, st>>>(lam_s, resid, K, n, lam_desc, info);
+  mark(3);
+  tri_check<<<1, 1024, 0, st>>>(lam_s, resid, reinterpret_cast<const int*>(vec[16]), K, n, lam_desc, info);
   HP_CHECK_LAUNCH("tri_check");
-  HP_CHECK_CUDA(d2h_small(hinfo, info, 12 * sizeof(double), st));
+  HP_CHECK_CUDA(d2h_small(hinfo, info, 16 * sizeof(double), st));
   count_launches(1);
   HP_CHECK_CUDA(cudaStreamSynchronize(st));
   if (diag) {
     diag[0] = hinfo[I_MINGAP];
     diag[1] = hinfo[I_MAXRES];
   }
-  if (hinfo[I_BAD] != 0.0 || !(hinfo[I_MINGAP] >= relgap_min) || !(hinfo[I_MAXRES] <= 1e-6)) return HP_OK;  // declined
+  mark(4);
+  if (trace)
+    fprintf(stderr, "[hp_syev_tri] K=%d getvec iterations max %.0f mean %.2f, min relgap %.2e, max resid %.2e\n", K,
+            hinfo[I_MAXIT], hinfo[I_SUMIT] / std::max(K, 1), hinfo[I_MINGAP], hinfo[I_MAXRES]);
+  if (hinfo[I_BAD] != 0.0 || !(hinfo[I_MINGAP] >= relgap_min) || !(hinfo[I_MAXRES] <= 1e-6)) {
+    report(4);
+    return HP_OK;  // declined
+  }
 
-  // W = Q Z: panels in reverse order, rows [j0, n) (row j0 of V_b is zero: keeps 16-byte alignment)
-  const int npanel = (int)ceil_div(n - 1, NB);
-  for (int b = npanel - 1; b >= 0; --b) {
-    const int j0 = b * NB;
-    const int j1 = std::min(j0 + NB, n - 1);
+  // W = Q Z: compact-WY blocks of BT reflectors in reverse order, rows [j0, n) (row j0 of V_b is
+  // zero: keeps 16-byte alignment).  Y = V_b^T Z; Y <- T Y by blocked back-substitution with the
+  // upper-triangular T^-1 (64-row diagonal blocks in shared memory, GEMMs above them); Z -= V_b Y.
+  const int nblock = (int)ceil_div(n - 1, BT);
+  for (int b = nblock - 1; b >= 0; --b) {
+    const int j0 = b * BT;
+    const int j1 = std::min(j0 + BT, n - 1);
     const int nbe = j1 - j0;
     const int64_t rows = n - j0;
     VecSet vb{Vall + j0 + (int64_t)j0 * lda, lda, nullptr};
     VecSet zb{W + j0, ldw, nullptr};
-    int rc = gemm_run(true, true, nbe, nbe, rows, vb, vb, true, 1.0, 0.0, S, NB, nullptr, nullptr, nullptr, 0, 0, gws,
+    int rc = gemm_run(true, true, nbe, nbe, rows, vb, vb, true, 1.0, 0.0, S, BT, nullptr, nullptr, nullptr, 0, 0, gws,
                       gwsb, st);
     if (rc) return rc;
-    tinv_build<<<(unsigned)ceil_div(nbe * nbe, 256), 256, 0, st>>>(S, NB, tau + j0, nbe);
+    tinv_build<<<(unsigned)ceil_div(nbe * nbe, 256), 256, 0, st>>>(S, BT, tau + j0, nbe);
     HP_CHECK_LAUNCH("tinv_build");
-    rc = gemm_run(true, true, nbe, K, rows, vb, zb, true, 1.0, 0.0, Y, NB, nullptr, nullptr, nullptr, 0, 0, gws, gwsb,
+    rc = gemm_run(true, true, nbe, K, rows, vb, zb, true, 1.0, 0.0, Y, BT, nullptr, nullptr, nullptr, 0, 0, gws, gwsb,
                   st);
     if (rc) return rc;
-    trsm_tinv<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(S, NB, nbe, Y, NB, K);
-    HP_CHECK_LAUNCH("trsm_tinv");
-    VecSet yb{Y, NB, nullptr};
+    for (int c0 = ((nbe - 1) / NB) * NB; c0 >= 0; c0 -= NB) {
+      const int c1 = std::min(c0 + NB, nbe);
+      if (c1 < nbe) {
+        VecSet ta{S + c0 + (int64_t)c1 * BT, BT, nullptr};
+        VecSet yl{Y + c1, BT, nullptr};
+        rc = gemm_run(false, true, c1 - c0, K, nbe - c1, ta, yl, true, -1.0, 1.0, Y + c0, BT, nullptr, nullptr,
+                      nullptr, 0, 0, gws, gwsb, st);
+        if (rc) return rc;
+      }
+      trsm_tinv<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(S + c0 + (int64_t)c0 * BT, BT, c1 - c0, Y + c0, BT, K);
+      HP_CHECK_LAUNCH("trsm_tinv");
+    }
+    VecSet yb{Y, BT, nullptr};
     rc = gemm_run(false, true, rows, K, nbe, vb, yb, true, -1.0, 1.0, W + j0, ldw, nullptr, nullptr, nullptr, 0, 0, gws,
                   gwsb, st);
     if (rc) return rc;
   }
+  mark(5);
+  report(5);
   *k_out = K;
   *status_out = 0;
   return HP_OK;

@@ -2,7 +2,7 @@
 d): node phases timed on the launching stream, mode counts, sigma and subspace differences between
 the two paths and against the exact POD (S = Q1 diag(sigma) Q2^T).
 
-    python tools/tri_study.py [d] [m] [repeats]
+    python tools/tri_study.py [d] [m] [repeats] [debug flags] [tri]
 """
 import os
 import sys
@@ -20,11 +20,17 @@ from oracle import hapod_oracle as O  # noqa: E402
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+if len(sys.argv) > 4:
+    from paper_1607_05210_b200 import _native as N  # noqa: E402
+    N.load().hp_set_debug(int(sys.argv[4]))
 wl = W.make(1, d=d, m=m)
 blk = H.SnapshotBlock(H.InnerProductSpace(d), wl.values)
 eps = 0.75 * wl.eps_star
 outs = {}
-for name, min_order in (("tri", 1024), ("jacobi", 1 << 30)):
+variants = (("tri", 1024), ("jacobi", 1 << 30))
+if len(sys.argv) > 5 and sys.argv[5] == "tri":
+    variants = variants[:1]
+for name, min_order in variants:
     D.TRI_MIN_ORDER = min_order
     for rep in range(reps):
         D.Profiler.reset(True)
@@ -39,6 +45,8 @@ for name, min_order in (("tri", 1024), ("jacobi", 1 << 30)):
         print(f"{name} rep {rep}: {dt * 1e3:.1f} ms modes={out.count} | {ph}", flush=True)
     print(name, "diag", out.diagnostics, D.LAST_TRI_DIAG if name == "tri" else "", flush=True)
     outs[name] = (out.count, np.asarray(out.sigmas), np.asarray(out.modes))
+if len(variants) < 2:
+    sys.exit(0)
 na, sa, ma = outs["tri"]
 nb, sb, mb = outs["jacobi"]
 n = min(na, nb)
