@@ -460,7 +460,17 @@ def chains_under_root(H, chains, per):
     return H.RootedTree(tuple(tuple(k) for k in children), 0)
 
 
-def gemm_roofline(summ, steps, step_ms, label):
+def hbm_peak_gbs():
+    """Measured copy bandwidth of this pool's B200 (MEASURED_PEAKS.json, driver-written); the
+    profiling recipe's fallback otherwise."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6500.0, "B200_PROFILING.md fallback"
+
+
+def gemm_roofline(summ, steps, step_ms, label, extra=None):
     """Roofline of the contraction family (Gram / block Gram / reconstruction / drift / CholQR /
     Ritz products) from the Profiler's CUDA-event records."""
     names = ("gram", "assemble", "drift", "reortho", "eigvec", "polish_q0", "polish_x", "polish_rr")
@@ -471,14 +481,33 @@ def gemm_roofline(summ, steps, step_ms, label):
     e_fl = sum(summ[k][2] for k in e_names if k in summ) / steps
     e_ms = sum(summ[k][1] for k in e_names if k in summ) / steps
     e_tf = e_fl / (e_ms * 1e-3) / 1e12 if e_ms else 0.0
+    eig = {"kernel": "pstrf + jac_round/jac_apply (block Jacobi; DMMA rotation products counted)",
+           "achieved": round(e_tf, 3), "frac": round(e_tf / FP64_PEAK_TFLOPS, 4),
+           "share_of_step": round(e_ms / step_ms, 4) if step_ms else None}
+    tri = (extra or {}).get("sytrd_panel")
+    if tri and tri[1] > 0.0:
+        # the large preconditioned eigenproblems go through hp_syev_tri: its dominant kernel is the
+        # HBM/L2-bound tridiagonalisation (one matrix-vector product per column)
+        peak, src = hbm_peak_gbs()
+        gbs = tri[2] / (tri[1] * 1e-3) / 1e9
+        t_ms = summ.get("eigensolve_tri", (0, 0.0, 0.0))[1] / steps
+        eig = {"kernel": "sytrd_panel (Householder tridiagonalisation of H = L^T L: one symmetric matrix-vector "
+                         "product per column, column dots over the trailing matrix; + syr2k GEMM per 64 columns)",
+               "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+               "peak_source": src, "algorithmic_bytes_per_solve": tri[2] / max(tri[0], 1),
+               "ms_per_solve": round(tri[1] / max(tri[0], 1), 3),
+               "note": "8 r^3 / 3 bytes of matrix reads per solve (full symmetric storage); the last ~40 % of the "
+                       "columns are L2-resident and latency-bound (two grid barriers per column)",
+               "eigensolve_tri_ms_per_step": round(t_ms, 3),
+               "share_of_step": round(t_ms / step_ms, 4) if step_ms else None,
+               "polish_jacobi": {"achieved_tflops": round(e_tf, 3), "frac": round(e_tf / FP64_PEAK_TFLOPS, 4),
+                                 "share_of_step": round(e_ms / step_ms, 4) if step_ms else None}}
     return {"bound": "tensor", "kernel": label, "achieved": round(tf, 3), "peak": FP64_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": round(tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
             "peak_source": "measured FP64 DMMA peak on this pool's B200 (tools/microbench/fp64_peak.cu, "
                            "profiles/r1_fp64_peak.txt); MEASURED_PEAKS.json carries no FP64 figure",
             "share_of_step": round(ms / step_ms, 4) if step_ms else None,
-            "eigensolver": {"kernel": "pstrf + jac_round/jac_apply (block Jacobi; DMMA rotation products counted)",
-                            "achieved": round(e_tf, 3), "frac": round(e_tf / FP64_PEAK_TFLOPS, 4),
-                            "share_of_step": round(e_ms / step_ms, 4) if step_ms else None},
+            "eigensolver": eig,
             "phases_ms_per_step": {k: round(v[1] / steps, 3) for k, v in sorted(summ.items())}}
 
 
@@ -666,6 +695,7 @@ def bench_resident(a, world, rank, local, torch, dist, H, D, DI, W, lib):
         return out
 
     summ_root = {}
+    tri_extra = {}
 
     def barrier():
         if world > 1:
@@ -698,6 +728,8 @@ def bench_resident(a, world, rank, local, torch, dist, H, D, DI, W, lib):
         summary = D.Profiler.summary() if profile else None
         if profile:
             summ_root = D.Profiler.summary(tag=tree.root)
+        if profile:
+            tri_extra.update(D.Profiler.extra)
         D.Profiler.reset(False)
         return ms, out, launches, summary
 
@@ -727,7 +759,7 @@ def bench_resident(a, world, rank, local, torch, dist, H, D, DI, W, lib):
     root_s = summ_root if summ_root else summ
     roofline = gemm_roofline(root_s, a.steps, step_ms,
                              "gemm_tma_kernel (FP64 DMMA GEMM engine: Gram SYRK, reconstruction, drift SYRK, CholQR "
-                             "TRMM, Ritz products) on the root node")
+                             "TRMM, Ritz products) on the root node", tri_extra)
     root_ms = sum(v[1] for v in root_s.values()) / a.steps
     roofline["root_share_of_step"] = round(root_ms / step_ms, 4)
     roofline["all_phases_ms_per_step (leaf wave overlapped)"] = {k: round(v[1] / a.steps, 3) for k, v in summ.items()}

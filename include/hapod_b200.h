@@ -136,12 +136,14 @@ int hp_syev_rows(const double* G, int64_t ldg, int64_t n, double* lam_desc, doub
  * eigenvalues descending, the rest zero; W (n x n, ldw even): eigenvectors in the first K columns.
  * status (host): 0 = done; 1 = declined -- the spectrum has a relative gap below relgap_min (the
  * eigenvectors of a cluster would not be orthogonal) or no definite representation exists -- and
- * the caller uses hp_syev instead; outputs are then not meaningful.  diag4 (nullable, host):
- * {smallest relative gap, largest relative residual, sigma, K}.  2 <= n <= hp_syev_tri_max_order(). */
+ * the caller uses hp_syev instead; outputs are then not meaningful.  diag8 (nullable, host):
+ * {smallest relative gap, largest relative residual, sigma, K, tridiagonalisation ms, tridiagonal
+ * eigensolve ms (CUDA events on the stream), max Rayleigh-quotient iterations, 0}.
+ * 2 <= n <= hp_syev_tri_max_order(). */
 int64_t hp_syev_tri_max_order(void);
 size_t hp_syev_tri_workspace_bytes(int64_t n);
 int hp_syev_tri(const double* H, int64_t ldh, int64_t n, double floor_rel, double relgap_min, double* lam_desc,
-                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag4, void* ws, size_t ws_bytes,
+                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag8, void* ws, size_t ws_bytes,
                 void* stream);
 
 /* K3 -- truncation (pod.py:278-289 with truncation_rank pod.py:190-205):

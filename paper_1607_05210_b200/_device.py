@@ -64,12 +64,14 @@ class Profiler:
 
     enabled = False
     records: list = []
+    extra: dict = {}           # kernel-level figures reported by the library itself: name -> (calls, ms, bytes)
     _tag = threading.local()   # the node a thread is evaluating (set by evaluate_node)
 
     @classmethod
     def reset(cls, enabled=True):
         cls.enabled = enabled
         cls.records = []
+        cls.extra = {}
 
     @classmethod
     def set_tag(cls, tag):
@@ -641,7 +643,7 @@ def _syev_tri(H: DevMat, r: int, floor_rel: float, st):
     ws = _ws(lib.hp_syev_tri_workspace_bytes(r))
     k = ctypes.c_int64(0)
     status = ctypes.c_int(1)
-    diag = (ctypes.c_double * 4)()
+    diag = (ctypes.c_double * 8)()
     ph = _phase("eigensolve_tri", 4.0 / 3.0 * float(r) ** 3)
     with ph:
         N.check(lib.hp_syev_tri(H.ptr, H.ld, r, float(floor_rel), TRI_RELGAP_MIN, lam.data_ptr(), W.ptr, W.ld,
@@ -649,7 +651,12 @@ def _syev_tri(H: DevMat, r: int, floor_rel: float, st):
                 "tridiagonal eigensolve")
         ph.flops += 4.0 * float(r) * r * k.value
     LAST_TRI_DIAG.update(order=r, count=int(k.value), status=int(status.value), min_relgap=diag[0],
-                         max_resid=diag[1], sigma=diag[2])
+                         max_resid=diag[1], sigma=diag[2], sytrd_ms=diag[4], tridiag_ms=diag[5], rqi_max=int(diag[6]))
+    if Profiler.enabled:
+        # the tridiagonalisation's own time and its algorithmic matrix reads (every column step reads
+        # the trailing matrix once: sum_j 8 (r - j)^2 = 8 r^3 / 3 bytes) for the HBM roofline
+        n_, ms_, b_ = Profiler.extra.get("sytrd_panel", (0, 0.0, 0.0))
+        Profiler.extra["sytrd_panel"] = (n_ + 1, ms_ + diag[4], b_ + 8.0 * float(r) ** 3 / 3.0)
     if status.value != 0:
         return None
     return lam, W
@@ -806,6 +813,53 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float, share: EigShare | 
     return EigVectors(lam_max, nkeep, n_modes, tail, sig_dev, Vn, sweeps)
 
 
+PRE_ORTH = True              # fold the CholQR factor into the coefficients when the drift allows it
+PRE_ORTH_MAX_DRIFT = 0.05    # one Cholesky-QR pass is exact to rounding well below kappa(U)^2 ~ 1.1
+
+
+def _coefficient_cholqr(G: DevMat, m: int, Vn: DevMat, sig_dev, n_modes: int, st):
+    """(drift', Vq): drift' = max |Sigma^-1 V^T G V Sigma^-1 - I|, the orthonormality drift of
+    U = S V / sigma (pod.py:245-247) evaluated through the node Gramian, and -- when
+    DRIFT_TOL < drift' <= PRE_ORTH_MAX_DRIFT -- the coefficients Vq = V Sigma^-1 L^-T with
+    C' = L L^T, so that S Vq are the re-orthonormalised modes (CholQR == the MGS sweep of
+    pod.py:227-237 in exact arithmetic).  Vq is None when no correction applies."""
+    lib = N.load()
+    T = DevMat.empty(m, n_modes)
+    C = DevMat.empty(n_modes, n_modes)
+    ws = _ws(max(lib.hp_gemm_workspace_bytes(m, n_modes, m, 0, 0), lib.hp_gemm_workspace_bytes(n_modes, n_modes, m, 1, 0)))
+    with _phase("pre_orth", 2.0 * m * m * n_modes + float(m) * n_modes * (n_modes + 1)):
+        N.check(lib.hp_gemm(0, 1, m, n_modes, m, G.vecset(), Vn.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None, None, 0, 0,
+                            ws.data_ptr(), ws.numel(), st), "G V")
+        N.check(lib.hp_gemm(1, 1, n_modes, n_modes, m, Vn.vecset(), T.vecset(), 1.0, 0.0, C.ptr, C.ld, None, None, None,
+                            1, 0, ws.data_ptr(), ws.numel(), st), "V^T G V")
+        rsig = 1.0 / sig_dev
+        N.check(lib.hp_scale(C.ptr, C.ld, n_modes, n_modes, None, sig_dev.data_ptr(), rsig.data_ptr(), C.ptr, C.ld, st),
+                "Sigma^-1 (V^T G V) Sigma^-1")
+        drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
+        N.check(lib.hp_gram_drift(C.ptr, C.ld, n_modes, drift_dev.data_ptr(), st), "coefficient drift")
+    del T, ws
+    pre = float(host_read(drift_dev)[0])
+    if not (DRIFT_TOL < pre <= PRE_ORTH_MAX_DRIFT):
+        return pre, None
+    Linv = DevMat.empty(n_modes, n_modes)
+    ws = _ws(lib.hp_chol_inverse_workspace_bytes(n_modes))
+    info = ctypes.c_int(0)
+    with _phase("pre_orth", float(n_modes) ** 3 / 3.0):
+        N.check(lib.hp_chol_inverse(C.ptr, C.ld, n_modes, Linv.ptr, Linv.ld, ctypes.byref(info), ws.data_ptr(), ws.numel(),
+                                    st), "coefficient CholQR factor")
+    del ws, C
+    if info.value != 0:
+        return pre, None
+    Vd = DevMat.empty(m, n_modes)
+    N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, None, None, rsig.data_ptr(), Vd.ptr, Vd.ld, st), "V / sigma")
+    Vq = DevMat.empty(m, n_modes)
+    ws = _ws(lib.hp_gemm_workspace_bytes(m, n_modes, n_modes, 0, 1))
+    with _phase("pre_orth", float(m) * n_modes * n_modes):
+        N.check(lib.hp_gemm(0, 0, m, n_modes, n_modes, Vd.vecset(), Linv.vecset(), 1.0, 0.0, Vq.ptr, Vq.ld, None, None, None,
+                            0, 1, ws.data_ptr(), ws.numel(), st), "(V / sigma) L^-T")
+    return pre, Vq
+
+
 def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
                        want_right: bool, sqrt_w=None) -> NodeOutput:
     """pod.py:278-293 on the device: eigensolve + truncation (eig_vectors), reconstruction,
@@ -825,37 +879,48 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     Vn = ev.Vn
     vs, scale, m2, keep = _concat_parts(parts)
     assert m2 == m
+    # Orthonormality of U = S V / sigma on the COEFFICIENT side: U^T U = Sigma^-1 (V^T G V) Sigma^-1
+    # (2 m^2 N + 2 m N^2 flops instead of d N^2).  When it shows the drift of pod.py:245-247 in the
+    # range where one Cholesky-QR pass is exact to rounding, the factor L^-T is folded into the
+    # coefficients, U = S (V Sigma^-1 L^-T): the same re-orthonormalised modes (same nested spans as
+    # the MGS sweep, pod.py:227-237) without a d x N x N triangular product on U.  The drift of the
+    # assembled U is still measured below and repaired by CholQR if it exceeds the tolerance.
+    pre_drift, Vq = None, None
+    if PRE_ORTH and G is not None and n_modes > 0:
+        pre_drift, Vq = _coefficient_cholqr(G, m, Vn, sig_dev, n_modes, st)
+    Vsrc = Vq if Vq is not None else Vn
     if scale is not None:
         Vs = DevMat.empty(m, n_modes)
-        N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
+        N.check(lib.hp_scale(Vsrc.ptr, Vsrc.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
                 "scale V")
     else:
-        Vs = Vn
+        Vs = Vsrc
+    div_ptr = None if Vq is not None else sig_dev.data_ptr()
     U = DevMat.empty(d, n_modes)
     live = [p for p in parts if p.mat.cols]
     if len(live) <= 1:
         ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
         with _phase("assemble", 2.0 * d * m * n_modes):
-            N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld,
+            N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, div_ptr, n_modes, U.ptr, U.ld,
                                     ws.data_ptr(), ws.numel(), st), "assemble")
     else:
         # a few column blocks (an incremental merge [Phi sigma | F]): U = sum_p S_p (V_p / sigma),
         # one plain-operand (TMA) GEMM per block accumulating into U -- no pointer table
-        rsig = 1.0 / sig_dev
+        rsig = (1.0 / sig_dev) if Vq is None else None
         ws = _ws(max(lib.hp_gemm_workspace_bytes(d, n_modes, p.mat.cols, 0, 0) for p in live))
         with _phase("assemble", 2.0 * d * m * n_modes):
             r0 = 0
             for i, p in enumerate(live):
                 c = p.mat.cols
                 Vp = DevMat.empty(c, n_modes)  # rows r0..r0+c of V / sigma, 16-byte aligned columns
-                N.check(lib.hp_scale(Vs.ptr + 8 * r0, Vs.ld, c, n_modes, None, None, rsig.data_ptr(), Vp.ptr, Vp.ld,
-                                     st), "V / sigma")
+                N.check(lib.hp_scale(Vs.ptr + 8 * r0, Vs.ld, c, n_modes, None, None,
+                                     rsig.data_ptr() if rsig is not None else None, Vp.ptr, Vp.ld, st), "V / sigma")
                 N.check(lib.hp_gemm(0, 1, d, n_modes, c, p.mat.vecset(), Vp.vecset(), 1.0, 0.0 if i == 0 else 1.0,
                                     U.ptr, U.ld, None, None, None, 0, 0, ws.data_ptr(), ws.numel(), st),
                         "assemble part")
                 r0 += c
         del rsig
-    del ws, Vs
+    del ws, Vs, Vq, Vsrc
     # drift = max |U^T W U - I| (U is in Euclidean coordinates when weighted)
     C = DevMat.empty(n_modes, n_modes)
     drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
@@ -865,7 +930,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                              st), "drift")
     del ws
     drift = float(host_read(drift_dev)[0])
-    reorthed = False
+    reorthed = div_ptr is None  # the Cholesky-QR factor was applied on the coefficient side
     if drift > DRIFT_TOL:
         ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
         passes = ctypes.c_int(0)
@@ -889,6 +954,8 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None,
                              R.ld if R is not None else 0, m if R is not None else 0, None, st), "signs")
     sig_host = host_read(sig_dev)
+    if div_ptr is None and pre_drift is not None:
+        drift = max(drift, pre_drift)  # report the drift of S V / sigma, the quantity pod.py:247 tests
     return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps, m)
 
 

@@ -255,11 +255,11 @@ int64_t hp_syev_tri_max_order(void) { return syev_tri_max_order(); }
 size_t hp_syev_tri_workspace_bytes(int64_t n) { return syev_tri_workspace_bytes(n); }
 
 int hp_syev_tri(const double* H, int64_t ldh, int64_t n, double floor_rel, double relgap_min, double* lam_desc,
-                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag4, void* ws, size_t ws_bytes,
+                double* W, int64_t ldw, int64_t* k_out, int* status, double* diag8, void* ws, size_t ws_bytes,
                 void* stream) {
   HP_REQUIRE(H && lam_desc && W && k_out && status && ws, "hp_syev_tri: null argument");
   HP_REQUIRE(floor_rel >= 0.0 && relgap_min >= 0.0, "hp_syev_tri: negative threshold");
-  return syev_tri_run(H, ldh, n, floor_rel, relgap_min, lam_desc, W, ldw, k_out, status, diag4, ws, ws_bytes,
+  return syev_tri_run(H, ldh, n, floor_rel, relgap_min, lam_desc, W, ldw, k_out, status, diag8, ws, ws_bytes,
                       (cudaStream_t)stream);
 }
 

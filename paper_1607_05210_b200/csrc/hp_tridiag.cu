@@ -102,6 +102,24 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// L2 residency control for the column sweeps while the trailing matrix is larger than L2: the last
+// columns of the matrix (they stay in the trailing matrix until the end) are loaded evict_last, the
+// rest evict_first, so ~88 MB of every sweep is served from L2 whatever the replacement policy
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double2 ld_l2hint(const double2* ptr, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+constexpr long long L2_KEEP_BYTES = 88ll << 20;
+
 // w_r = tau (A v - V W^T v - W V^T v)_r + alpha' v_r: one expression shared by the row owners and by
 // the CTA-local copy of row j+1, so both produce the same bits
 __device__ __forceinline__ double w_entry(double tau, double av, double acc, double alpha_p, double v) {
@@ -210,6 +228,10 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
         // serpentine: odd columns walk their chunk backwards, so a sweep starts on the part of the
         // trailing matrix the previous sweep left in L2
         const int ngroup = (t1 - t0 + 3) >> 2;
+        // trailing matrix larger than L2: pin its last columns (task indices >= keep_from)
+        const bool hinted = (long long)nr * len * 8 > (112ll << 20);
+        const int keep_from = hinted ? max(0, nr - (int)(L2_KEEP_BYTES / (8ll * len))) : 0;
+        const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
         for (int g = 0; g < ngroup; ++g) {
           const int tb = t0 + 4 * ((j & 1) ? ngroup - 1 - g : g);
           const double2* q0 = task_ptr(tb);
@@ -217,21 +239,45 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
           const double2* q2 = task_ptr(tb + 2);
           const double2* q3 = task_ptr(tb + 3);
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          if (hinted) {
+            // task index >= keep_from: a persisting column of A, or a panel column (read every step)
+            const uint64_t p0 = min(tb, t1 - 1) >= keep_from ? pol_keep : pol_stream;
+            const uint64_t p1 = min(tb + 1, t1 - 1) >= keep_from ? pol_keep : pol_stream;
+            const uint64_t p2 = min(tb + 2, t1 - 1) >= keep_from ? pol_keep : pol_stream;
+            const uint64_t p3 = min(tb + 3, t1 - 1) >= keep_from ? pol_keep : pol_stream;
 #pragma unroll 2
-          for (int q = tid; q < len2; q += TT) {
-            const double2 xv = xs2[q];
-            const double2 v0 = __ldcg(q0 + q);
-            const double2 v1 = __ldcg(q1 + q);
-            const double2 v2 = __ldcg(q2 + q);
-            const double2 v3 = __ldcg(q3 + q);
-            a0 = fma(v0.x, xv.x, a0);
-            a0 = fma(v0.y, xv.y, a0);
-            a1 = fma(v1.x, xv.x, a1);
-            a1 = fma(v1.y, xv.y, a1);
-            a2 = fma(v2.x, xv.x, a2);
-            a2 = fma(v2.y, xv.y, a2);
-            a3 = fma(v3.x, xv.x, a3);
-            a3 = fma(v3.y, xv.y, a3);
+            for (int q = tid; q < len2; q += TT) {
+              const double2 xv = xs2[q];
+              const double2 v0 = ld_l2hint(q0 + q, p0);
+              const double2 v1 = ld_l2hint(q1 + q, p1);
+              const double2 v2 = ld_l2hint(q2 + q, p2);
+              const double2 v3 = ld_l2hint(q3 + q, p3);
+              a0 = fma(v0.x, xv.x, a0);
+              a0 = fma(v0.y, xv.y, a0);
+              a1 = fma(v1.x, xv.x, a1);
+              a1 = fma(v1.y, xv.y, a1);
+              a2 = fma(v2.x, xv.x, a2);
+              a2 = fma(v2.y, xv.y, a2);
+              a3 = fma(v3.x, xv.x, a3);
+              a3 = fma(v3.y, xv.y, a3);
+            }
+          } else {
+#pragma unroll 2
+            for (int q = tid; q < len2; q += TT) {
+              const double2 xv = xs2[q];
+              const double2 v0 = __ldcg(q0 + q);
+              const double2 v1 = __ldcg(q1 + q);
+              const double2 v2 = __ldcg(q2 + q);
+              const double2 v3 = __ldcg(q3 + q);
+              a0 = fma(v0.x, xv.x, a0);
+              a0 = fma(v0.y, xv.y, a0);
+              a1 = fma(v1.x, xv.x, a1);
+              a1 = fma(v1.y, xv.y, a1);
+              a2 = fma(v2.x, xv.x, a2);
+              a2 = fma(v2.y, xv.y, a2);
+              a3 = fma(v3.x, xv.x, a3);
+              a3 = fma(v3.y, xv.y, a3);
+            }
           }
           a0 = warp_sum(a0);
           a1 = warp_sum(a1);
@@ -269,10 +315,33 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
       xa = block_sum(xa, rbuf);
       if (tid == 0) p.red[cta] = xa;
     }
+    // Prefetch for P3: this thread's panel row, row j+1 of the panel and column j+1 of A depend on
+    // nothing this column's dots produce, so their L2 round trip overlaps the grid barrier
+    auto load_row = [&](int r, bool valid, double (&vv)[8], double (&ww)[8], double& anext) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = sub8 + 8 * u;
+        const bool on = valid && c < i;
+        vv[u] = on ? __ldcg(Pv + r + (int64_t)c * ldp) : 0.0;
+        ww[u] = on ? __ldcg(Pw + r + (int64_t)c * ldp) : 0.0;
+      }
+      anext = valid ? p.A[r + (int64_t)(j + 1) * p.lda] : 0.0;
+    };
+    double vv[8], ww[8], anext;
+    const int r_first = j + 1 + wbase8 + (lane >> 3);
+    load_row(r_first, r_first < n, vv, ww, anext);
+    double rv = 0.0, rw = 0.0;
+    if (tid < i) {
+      rv = __ldcg(Pv + (j + 1) + (int64_t)tid * ldp);
+      rw = __ldcg(Pw + (j + 1) + (int64_t)tid * ldp);
+    }
+    const double a11 = p.A[(j + 1) + (int64_t)(j + 1) * p.lda];
     if (prof) tp[1] = gtime();
     grid.sync();
     if (prof) tp[2] = gtime();
     // ------------------------------------------------------------------ P3: reflector, w, next column
+    const double y1 = __ldcg(p.y + j + 1);
+    double yr = r_first < n ? __ldcg(p.y + r_first) : 0.0;
     double tau, beta, s, t;
     {
       const double xnorm = sqrt(ssq);
@@ -293,8 +362,6 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
       p.tau[j] = tau;
     }
     if (tid < i) {
-      const double rv = __ldcg(Pv + (j + 1) + (int64_t)tid * ldp);
-      const double rw = __ldcg(Pw + (j + 1) + (int64_t)tid * ldp);
       rowV[tid] = rv;
       rowW[tid] = rw;
       cV[tid] = s * __ldcg(p.pxv + tid) + t * rv;
@@ -327,34 +394,26 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
     }
     __syncthreads();
     // w^T v = tau (v^T A v - 2 (V^T v).(W^T v)) with v = s x + t e_1: no grid-wide reduction of its own
-    const double y1 = __ldcg(p.y + j + 1);
-    const double a11 = p.A[(j + 1) + (int64_t)(j + 1) * p.lda];
     const double vAv = s * s * scal[0] + 2.0 * s * t * y1 + t * t * a11;
     const double alpha_p = -0.5 * tau * (tau * (vAv - 2.0 * scal[1]));
     const double vj1 = (tau == 0.0) ? 0.0 : 1.0;
     const double wrow = w_entry(tau, s * y1 + t * a11, scal[2], alpha_p, vj1);  // W[j+1, i]
     const bool do_next = (j + 1 < p.j1) || (p.j1 == n - 1);
-    for (int rb = j + 1 + wbase8; rb < n; rb += wstride8) {  // 8 lanes per row, every panel load in flight at once
+    for (int rb = j + 1 + wbase8; rb < n; rb += wstride8) {  // 8 lanes per row (one pass for n <= 9472)
       const int r = rb + (lane >> 3);
       const bool valid = r < n;
+      if (rb != j + 1 + wbase8) {
+        load_row(r, valid, vv, ww, anext);
+        yr = valid ? __ldcg(p.y + r) : 0.0;
+      }
       double acc1 = 0.0, acc2 = 0.0;
-      {
-        double vv[8], ww[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = sub8 + 8 * u;
-          const bool on = valid && c < i;
-          vv[u] = on ? __ldcg(Pv + r + (int64_t)c * ldp) : 0.0;
-          ww[u] = on ? __ldcg(Pw + r + (int64_t)c * ldp) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = sub8 + 8 * u;  // c < NB: the coefficient arrays are zero past i
-          acc1 = fma(vv[u], cW[c], acc1);
-          acc1 = fma(ww[u], cV[c], acc1);
-          acc2 = fma(vv[u], rowW[c], acc2);
-          acc2 = fma(ww[u], rowV[c], acc2);
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int c = sub8 + 8 * u;  // c < NB: the coefficient arrays are zero past i
+        acc1 = fma(vv[u], cW[c], acc1);
+        acc1 = fma(ww[u], cV[c], acc1);
+        acc2 = fma(vv[u], rowW[c], acc2);
+        acc2 = fma(ww[u], rowV[c], acc2);
       }
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) {
@@ -363,8 +422,7 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
       }
       if (valid && sub8 == 0) {
         const double v = (tau == 0.0) ? 0.0 : ((r == j + 1) ? 1.0 : s * xs[r - r0]);
-        const double anext = p.A[r + (int64_t)(j + 1) * p.lda];
-        const double w = w_entry(tau, s * __ldcg(p.y + r) + t * anext, acc1, alpha_p, v);
+        const double w = w_entry(tau, s * yr + t * anext, acc1, alpha_p, v);
         Pv[r + (int64_t)i * ldp] = v;
         Qv[r + (int64_t)i * ldp] = v;
         p.Vall[r + (int64_t)j * p.ldv] = v;
@@ -821,7 +879,8 @@ size_t syev_tri_workspace_bytes(int64_t n) {
 // lam_desc[0..K) descending (the rest zeroed), eigenvectors in the first K columns of W (n x n).
 // status_out: 0 = done; 1 = declined (clustered spectrum, relative gap below relgap_min, or no
 // definite root representation) -- W / lam_desc are then not meaningful and the caller falls back
-// to hp_syev.  diag (nullable, host, 4 doubles): min relative gap, max relative residual, sigma, K.
+// to hp_syev.  diag (nullable, host, 8 doubles): min relative gap, max relative residual, sigma, K,
+// sytrd stage ms, tridiagonal stage ms, max Rayleigh-quotient iterations, 0.
 int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, double relgap_min, double* lam_desc,
                  double* W, int64_t ldw, int64_t* k_out, int* status_out, double* diag, void* ws, size_t ws_bytes,
                  cudaStream_t st) {
@@ -861,25 +920,32 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   void* gws = base + o;
   const size_t gwsb = ws_bytes - o;
 
-  // stage timing (hp_set_debug bit 3): CUDA events on the launching stream, printed at the end
+  // stage timing: CUDA events on the launching stream (diag receives the sytrd / tridiagonal stage
+  // times for the caller's roofline; hp_set_debug bit 3 prints every stage)
   const bool trace = (debug_flags() & DBG_TRI_TRACE) != 0;
-  cudaEvent_t ev[6] = {};
+  struct Events {
+    cudaEvent_t ev[6] = {};
+    ~Events() {
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } evs;
+  cudaEvent_t* ev = evs.ev;
   auto mark = [&](int i) {
-    if (trace && (ev[i] || cudaEventCreate(&ev[i]) == cudaSuccess)) cudaEventRecord(ev[i], st);
+    if (ev[i] || cudaEventCreate(&ev[i]) == cudaSuccess) cudaEventRecord(ev[i], st);
+  };
+  auto elapsed = [&](int a, int b) -> double {
+    float ms = 0.f;
+    if (!ev[a] || !ev[b] || cudaEventElapsedTime(&ms, ev[a], ev[b]) != cudaSuccess) return 0.0;
+    return (double)ms;
   };
   auto report = [&](int last) {
     if (!trace) return;
     cudaEventSynchronize(ev[last]);
     static const char* names[] = {"sytrd", "prepare", "bisect+getvec", "check", "backtransform"};
     fprintf(stderr, "[hp_syev_tri] n=%d", n);
-    for (int i = 0; i < last; ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-      fprintf(stderr, " %s=%.2fms", names[i], ms);
-    }
+    for (int i = 0; i < last; ++i) fprintf(stderr, " %s=%.2fms", names[i], elapsed(i, i + 1));
     fprintf(stderr, "\n");
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
   };
   mark(0);
   copy_in<<<(unsigned)ceil_div(lda * n, 256), 256, 0, st>>>(H, ldh, n, A, lda);
@@ -973,10 +1039,10 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   const bool ok = hinfo[I_OK] != 0.0;
   const int K = (int)hinfo[I_K];
   if (diag) {
-    diag[0] = 0.0;
-    diag[1] = 0.0;
+    for (int q = 0; q < 8; ++q) diag[q] = 0.0;
     diag[2] = hinfo[I_SIGMA];
     diag[3] = (double)K;
+    diag[4] = elapsed(0, 1);
   }
   mark(2);
   if (!ok || K <= 0) report(2);
@@ -1001,6 +1067,8 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
   if (diag) {
     diag[0] = hinfo[I_MINGAP];
     diag[1] = hinfo[I_MAXRES];
+    diag[5] = elapsed(1, 3);
+    diag[6] = hinfo[I_MAXIT];
   }
   mark(4);
   if (trace)

@@ -311,7 +311,7 @@ def _tri_solve(g, floor_rel, relgap_min=1e-9):
     w = ws(lib.hp_syev_tri_workspace_bytes(n))
     k = ctypes.c_int64(0)
     status = ctypes.c_int(1)
-    diag = (ctypes.c_double * 4)()
+    diag = (ctypes.c_double * 8)()
     N.check(lib.hp_syev_tri(G.ptr, G.ld, n, floor_rel, relgap_min, lam_d.data_ptr(), W.ptr, W.ld, ctypes.byref(k),
                             ctypes.byref(status), diag, w.data_ptr(), w.numel(), st()), "syev_tri")
     torch.cuda.synchronize()
