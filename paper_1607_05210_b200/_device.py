@@ -526,6 +526,7 @@ def gram_block(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int):
 
 
 BJORCK_MAX_DRIFT = 0.05  # Newton-Schulz: quadratic from here
+POLISH_ORTH_TOL = 1e-10  # orthonormality the Ritz basis needs (eigenvalues move by at most this, relatively)
 
 
 def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
@@ -543,9 +544,22 @@ def _orthonormalise_basis(X: DevMat, ws, st, ph) -> float:
     if drift > BJORCK_MAX_DRIFT:
         rws = _ws(lib.hp_reortho_workspace_bytes(m, K))
         passes = ctypes.c_int(0)
-        N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, drift, ctypes.byref(passes),
+        # The max-norm drift of X = G Q0 / lambda is O(1) (its trailing columns are amplified along the
+        # larger eigenvectors), but kappa(X) stays ~10: ONE Cholesky-QR pass leaves u kappa^2 ~ 1e-13.
+        # hp_reorthonormalize takes a single pass for a declared drift <= 0.1; the result is measured
+        # and only a basis still above POLISH_ORTH_TOL gets the second pass.
+        N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, min(drift, 0.1), ctypes.byref(passes),
                                         rws.data_ptr(), rws.numel(), st), "orthonormalise X")
         ph.flops += passes.value * 2.0 * m * K * K
+        if passes.value == 1:
+            N.check(lib.hp_drift(X.ptr, X.ld, m, K, C.ptr, C.ld, drift_dev.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                    "X^T X")
+            ph.flops += float(m) * K * (K + 1)
+            drift1 = float(host_read(drift_dev)[0])
+            if not (drift1 <= POLISH_ORTH_TOL):
+                N.check(lib.hp_reorthonormalize(X.ptr, X.ld, m, K, C.ptr, C.ld, drift1, ctypes.byref(passes),
+                                                rws.data_ptr(), rws.numel(), st), "orthonormalise X (second pass)")
+                ph.flops += passes.value * 2.0 * m * K * K
         return drift0
     Y = DevMat.empty(m, K)
     orig = X
@@ -813,53 +827,6 @@ def eig_vectors(G: DevMat, m: int, eps: float, cutoff: float, share: EigShare | 
     return EigVectors(lam_max, nkeep, n_modes, tail, sig_dev, Vn, sweeps)
 
 
-PRE_ORTH = True              # fold the CholQR factor into the coefficients when the drift allows it
-PRE_ORTH_MAX_DRIFT = 0.05    # one Cholesky-QR pass is exact to rounding well below kappa(U)^2 ~ 1.1
-
-
-def _coefficient_cholqr(G: DevMat, m: int, Vn: DevMat, sig_dev, n_modes: int, st):
-    """(drift', Vq): drift' = max |Sigma^-1 V^T G V Sigma^-1 - I|, the orthonormality drift of
-    U = S V / sigma (pod.py:245-247) evaluated through the node Gramian, and -- when
-    DRIFT_TOL < drift' <= PRE_ORTH_MAX_DRIFT -- the coefficients Vq = V Sigma^-1 L^-T with
-    C' = L L^T, so that S Vq are the re-orthonormalised modes (CholQR == the MGS sweep of
-    pod.py:227-237 in exact arithmetic).  Vq is None when no correction applies."""
-    lib = N.load()
-    T = DevMat.empty(m, n_modes)
-    C = DevMat.empty(n_modes, n_modes)
-    ws = _ws(max(lib.hp_gemm_workspace_bytes(m, n_modes, m, 0, 0), lib.hp_gemm_workspace_bytes(n_modes, n_modes, m, 1, 0)))
-    with _phase("pre_orth", 2.0 * m * m * n_modes + float(m) * n_modes * (n_modes + 1)):
-        N.check(lib.hp_gemm(0, 1, m, n_modes, m, G.vecset(), Vn.vecset(), 1.0, 0.0, T.ptr, T.ld, None, None, None, 0, 0,
-                            ws.data_ptr(), ws.numel(), st), "G V")
-        N.check(lib.hp_gemm(1, 1, n_modes, n_modes, m, Vn.vecset(), T.vecset(), 1.0, 0.0, C.ptr, C.ld, None, None, None,
-                            1, 0, ws.data_ptr(), ws.numel(), st), "V^T G V")
-        rsig = 1.0 / sig_dev
-        N.check(lib.hp_scale(C.ptr, C.ld, n_modes, n_modes, None, sig_dev.data_ptr(), rsig.data_ptr(), C.ptr, C.ld, st),
-                "Sigma^-1 (V^T G V) Sigma^-1")
-        drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
-        N.check(lib.hp_gram_drift(C.ptr, C.ld, n_modes, drift_dev.data_ptr(), st), "coefficient drift")
-    del T, ws
-    pre = float(host_read(drift_dev)[0])
-    if not (DRIFT_TOL < pre <= PRE_ORTH_MAX_DRIFT):
-        return pre, None
-    Linv = DevMat.empty(n_modes, n_modes)
-    ws = _ws(lib.hp_chol_inverse_workspace_bytes(n_modes))
-    info = ctypes.c_int(0)
-    with _phase("pre_orth", float(n_modes) ** 3 / 3.0):
-        N.check(lib.hp_chol_inverse(C.ptr, C.ld, n_modes, Linv.ptr, Linv.ld, ctypes.byref(info), ws.data_ptr(), ws.numel(),
-                                    st), "coefficient CholQR factor")
-    del ws, C
-    if info.value != 0:
-        return pre, None
-    Vd = DevMat.empty(m, n_modes)
-    N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, None, None, rsig.data_ptr(), Vd.ptr, Vd.ld, st), "V / sigma")
-    Vq = DevMat.empty(m, n_modes)
-    ws = _ws(lib.hp_gemm_workspace_bytes(m, n_modes, n_modes, 0, 1))
-    with _phase("pre_orth", float(m) * n_modes * n_modes):
-        N.check(lib.hp_gemm(0, 0, m, n_modes, n_modes, Vd.vecset(), Linv.vecset(), 1.0, 0.0, Vq.ptr, Vq.ld, None, None, None,
-                            0, 1, ws.data_ptr(), ws.numel(), st), "(V / sigma) L^-T")
-    return pre, Vq
-
-
 def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float, cutoff: float,
                        want_right: bool, sqrt_w=None) -> NodeOutput:
     """pod.py:278-293 on the device: eigensolve + truncation (eig_vectors), reconstruction,
@@ -879,48 +846,37 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     Vn = ev.Vn
     vs, scale, m2, keep = _concat_parts(parts)
     assert m2 == m
-    # Orthonormality of U = S V / sigma on the COEFFICIENT side: U^T U = Sigma^-1 (V^T G V) Sigma^-1
-    # (2 m^2 N + 2 m N^2 flops instead of d N^2).  When it shows the drift of pod.py:245-247 in the
-    # range where one Cholesky-QR pass is exact to rounding, the factor L^-T is folded into the
-    # coefficients, U = S (V Sigma^-1 L^-T): the same re-orthonormalised modes (same nested spans as
-    # the MGS sweep, pod.py:227-237) without a d x N x N triangular product on U.  The drift of the
-    # assembled U is still measured below and repaired by CholQR if it exceeds the tolerance.
-    pre_drift, Vq = None, None
-    if PRE_ORTH and G is not None and n_modes > 0:
-        pre_drift, Vq = _coefficient_cholqr(G, m, Vn, sig_dev, n_modes, st)
-    Vsrc = Vq if Vq is not None else Vn
     if scale is not None:
         Vs = DevMat.empty(m, n_modes)
-        N.check(lib.hp_scale(Vsrc.ptr, Vsrc.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
+        N.check(lib.hp_scale(Vn.ptr, Vn.ld, m, n_modes, scale.data_ptr(), None, None, Vs.ptr, Vs.ld, st),
                 "scale V")
     else:
-        Vs = Vsrc
-    div_ptr = None if Vq is not None else sig_dev.data_ptr()
+        Vs = Vn
     U = DevMat.empty(d, n_modes)
     live = [p for p in parts if p.mat.cols]
     if len(live) <= 1:
         ws = _ws(lib.hp_assemble_workspace_bytes(d, m, n_modes))
         with _phase("assemble", 2.0 * d * m * n_modes):
-            N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, div_ptr, n_modes, U.ptr, U.ld,
+            N.check(lib.hp_assemble(vs, d, m, Vs.ptr, Vs.ld, sig_dev.data_ptr(), n_modes, U.ptr, U.ld,
                                     ws.data_ptr(), ws.numel(), st), "assemble")
     else:
         # a few column blocks (an incremental merge [Phi sigma | F]): U = sum_p S_p (V_p / sigma),
         # one plain-operand (TMA) GEMM per block accumulating into U -- no pointer table
-        rsig = (1.0 / sig_dev) if Vq is None else None
+        rsig = 1.0 / sig_dev
         ws = _ws(max(lib.hp_gemm_workspace_bytes(d, n_modes, p.mat.cols, 0, 0) for p in live))
         with _phase("assemble", 2.0 * d * m * n_modes):
             r0 = 0
             for i, p in enumerate(live):
                 c = p.mat.cols
                 Vp = DevMat.empty(c, n_modes)  # rows r0..r0+c of V / sigma, 16-byte aligned columns
-                N.check(lib.hp_scale(Vs.ptr + 8 * r0, Vs.ld, c, n_modes, None, None,
-                                     rsig.data_ptr() if rsig is not None else None, Vp.ptr, Vp.ld, st), "V / sigma")
+                N.check(lib.hp_scale(Vs.ptr + 8 * r0, Vs.ld, c, n_modes, None, None, rsig.data_ptr(), Vp.ptr, Vp.ld,
+                                     st), "V / sigma")
                 N.check(lib.hp_gemm(0, 1, d, n_modes, c, p.mat.vecset(), Vp.vecset(), 1.0, 0.0 if i == 0 else 1.0,
                                     U.ptr, U.ld, None, None, None, 0, 0, ws.data_ptr(), ws.numel(), st),
                         "assemble part")
                 r0 += c
         del rsig
-    del ws, Vs, Vq, Vsrc
+    del ws, Vs
     # drift = max |U^T W U - I| (U is in Euclidean coordinates when weighted)
     C = DevMat.empty(n_modes, n_modes)
     drift_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
@@ -930,7 +886,7 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
                              st), "drift")
     del ws
     drift = float(host_read(drift_dev)[0])
-    reorthed = div_ptr is None  # the Cholesky-QR factor was applied on the coefficient side
+    reorthed = False
     if drift > DRIFT_TOL:
         ws = _ws(lib.hp_reortho_workspace_bytes(d, n_modes))
         passes = ctypes.c_int(0)
@@ -954,8 +910,6 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
         N.check(lib.hp_signs(U.ptr, U.ld, d, n_modes, R.ptr if R is not None else None,
                              R.ld if R is not None else 0, m if R is not None else 0, None, st), "signs")
     sig_host = host_read(sig_dev)
-    if div_ptr is None and pre_drift is not None:
-        drift = max(drift, pre_drift)  # report the drift of S V / sigma, the quantity pod.py:247 tests
     return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps, m)
 
 

@@ -102,24 +102,6 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-// L2 residency control for the column sweeps while the trailing matrix is larger than L2: the last
-// columns of the matrix (they stay in the trailing matrix until the end) are loaded evict_last, the
-// rest evict_first, so ~88 MB of every sweep is served from L2 whatever the replacement policy
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-  uint64_t pol;
-  if (keep)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ double2 ld_l2hint(const double2* ptr, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
-  return v;
-}
-constexpr long long L2_KEEP_BYTES = 88ll << 20;
-
 // w_r = tau (A v - V W^T v - W V^T v)_r + alpha' v_r: one expression shared by the row owners and by
 // the CTA-local copy of row j+1, so both produce the same bits
 __device__ __forceinline__ double w_entry(double tau, double av, double acc, double alpha_p, double v) {
@@ -228,10 +210,6 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
         // serpentine: odd columns walk their chunk backwards, so a sweep starts on the part of the
         // trailing matrix the previous sweep left in L2
         const int ngroup = (t1 - t0 + 3) >> 2;
-        // trailing matrix larger than L2: pin its last columns (task indices >= keep_from)
-        const bool hinted = (long long)nr * len * 8 > (112ll << 20);
-        const int keep_from = hinted ? max(0, nr - (int)(L2_KEEP_BYTES / (8ll * len))) : 0;
-        const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
         for (int g = 0; g < ngroup; ++g) {
           const int tb = t0 + 4 * ((j & 1) ? ngroup - 1 - g : g);
           const double2* q0 = task_ptr(tb);
@@ -239,29 +217,6 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
           const double2* q2 = task_ptr(tb + 2);
           const double2* q3 = task_ptr(tb + 3);
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          if (hinted) {
-            // task index >= keep_from: a persisting column of A, or a panel column (read every step)
-            const uint64_t p0 = min(tb, t1 - 1) >= keep_from ? pol_keep : pol_stream;
-            const uint64_t p1 = min(tb + 1, t1 - 1) >= keep_from ? pol_keep : pol_stream;
-            const uint64_t p2 = min(tb + 2, t1 - 1) >= keep_from ? pol_keep : pol_stream;
-            const uint64_t p3 = min(tb + 3, t1 - 1) >= keep_from ? pol_keep : pol_stream;
-#pragma unroll 2
-            for (int q = tid; q < len2; q += TT) {
-              const double2 xv = xs2[q];
-              const double2 v0 = ld_l2hint(q0 + q, p0);
-              const double2 v1 = ld_l2hint(q1 + q, p1);
-              const double2 v2 = ld_l2hint(q2 + q, p2);
-              const double2 v3 = ld_l2hint(q3 + q, p3);
-              a0 = fma(v0.x, xv.x, a0);
-              a0 = fma(v0.y, xv.y, a0);
-              a1 = fma(v1.x, xv.x, a1);
-              a1 = fma(v1.y, xv.y, a1);
-              a2 = fma(v2.x, xv.x, a2);
-              a2 = fma(v2.y, xv.y, a2);
-              a3 = fma(v3.x, xv.x, a3);
-              a3 = fma(v3.y, xv.y, a3);
-            }
-          } else {
 #pragma unroll 2
             for (int q = tid; q < len2; q += TT) {
               const double2 xv = xs2[q];
@@ -278,7 +233,6 @@ __global__ void __launch_bounds__(TT, 1) sytrd_panel(Panel p) {
               a3 = fma(v3.x, xv.x, a3);
               a3 = fma(v3.y, xv.y, a3);
             }
-          }
           a0 = warp_sum(a0);
           a1 = warp_sum(a1);
           a2 = warp_sum(a2);

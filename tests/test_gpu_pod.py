@@ -339,41 +339,3 @@ def test_space_gram_rejects_mismatched_rows():
     sp = H.InnerProductSpace(10)
     with pytest.raises(ValueError):
         sp.gram(np.ones((10, 2)), np.ones((11, 2)))
-
-
-def test_coefficient_side_cholqr_equals_the_standard_path():
-    """The Cholesky-QR factor folded into the coefficients (U = S V Sigma^-1 L^-T, _device.
-    _coefficient_cholqr) gives the modes the explicit re-orthonormalisation of U gives (the MGS
-    sweep of pod.py:227-237): same counts and sigma (bitwise -- the spectrum is untouched), same
-    nested spans, orthonormal within the reference's own tolerance (pod.py:247), and the same
-    diagnostics (drift of S V / sigma, reorthonormalized)."""
-    from paper_1607_05210_b200 import _device as D
-    rng = np.random.default_rng(5)
-    d, m = 4000, 300
-    q1, _ = np.linalg.qr(rng.standard_normal((d, m)))
-    q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
-    vals = (q1 * 10.0 ** (-6.0 * np.arange(m) / (m - 1))) @ q2.T
-    blk = H.SnapshotBlock(euclid(d), vals)
-    eps = 1e-7 * float(np.linalg.norm(vals))
-    outs = {}
-    try:
-        for flag in (True, False):
-            D.PRE_ORTH = flag
-            outs[flag] = H.pod(blk, eps, want_right=True)
-    finally:
-        D.PRE_ORTH = True
-    a, b = outs[True], outs[False]
-    print("pre-orth drift", a.diagnostics["drift"], "standard drift", b.diagnostics["drift"])
-    assert b.diagnostics["reorthonormalized"] and a.diagnostics["reorthonormalized"]
-    assert a.count == b.count and a.count > 100
-    assert np.array_equal(a.sigmas, b.sigmas)
-    assert a.diagnostics["drift"] == pytest.approx(b.diagnostics["drift"], rel=1e-2)
-    ga = a.modes.T @ a.modes
-    assert np.max(np.abs(ga - np.eye(a.count))) <= 1e-8
-    # nested spans: every leading block of modes spans the same space
-    for k in (a.count // 3, a.count):
-        s = angles(a.modes[:, :k], b.modes[:, :k])
-        assert s.max() < 1e-7, (k, s.max())
-    assert np.allclose(a.right, b.right, rtol=0, atol=1e-12)
-    ref = O.pod(vals, eps)
-    assert a.count == ref.count
