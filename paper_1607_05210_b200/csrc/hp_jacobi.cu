@@ -50,6 +50,7 @@ constexpr int PS = 2 * BW;    // local problem size
 constexpr int LS = PS + 1;    // local smem stride
 constexpr int TS = PS + 4;    // apply-kernel smem stride (= 4 mod 16: conflict-free DMMA fragments)
 constexpr int AT = 256;       // apply threads
+constexpr int64_t GRAPH_MAX_ORDER = 2048;  // padded orders up to this replay their sweeps as CUDA graphs
 
 struct Params {
   double* G;          // n_p x n_p, ld = n_p
@@ -842,46 +843,95 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
   cudaEvent_t ev[3];
   if (trace > 1)
     for (auto& e : ev) cudaEventCreate(&e);
-  HP_CHECK_CUDA(zero_async(p.tile_mark, (size_t)npairs * (npairs + 1) / 2 * 4, st));
   const unsigned needed_grid = (unsigned)std::min<int64_t>(2 * (int64_t)npairs, 2 * (int64_t)nsm);  // one task per CTA (2 per SM)
   // small problems (leaves, merges) get a grid sized to their work -- about four apply tasks per
   // CTA, never fewer CTAs than local solves -- so that concurrent node streams do not flood the
   // SMs with idle apply CTAs; large ones use every SM twice
   const unsigned rest_grid =
       (unsigned)std::min<int64_t>(std::max<int64_t>(npairs, ceil_div(napply, 4)), 2 * (int64_t)nsm);
-  int stamp = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    cudaError_t e = zero_async(p.counter, 24, st);
-    if (e != cudaSuccess) break;
+  // One sweep = 2 R + 4 dependent launches with the same arguments every sweep (round stamps restart at 1;
+  // the tile marks are cleared per sweep).  Small problems (leaves, chain merges: kernels of a few
+  // microseconds, 16 host threads launching at once in a leaf wave) replay the sweep as a CUDA graph
+  // captured on this thread's side stream, so a sweep costs one launch call instead of ~30-130.
+  const int R = L.nb - 1;
+  auto enqueue_sweep = [&](cudaStream_t ls) -> cudaError_t {
+    cudaError_t e = zero_async(p.counter, 24, ls);
+    if (e != cudaSuccess) return e;
+    e = zero_async(p.tile_mark, (size_t)npairs * (npairs + 1) / 2 * 4, ls);
+    if (e != cudaSuccess) return e;
     // Per round r: needed(r), then ONE fused launch in which CTAs 0..npairs-1 solve the local
     // problems of round r+1 before joining the dynamically scheduled rest of round r's apply.
-    const int R = L.nb - 1;
     auto round_params = [&](int r) {
       Params q = p;
       q.round = r;
       q.W = W_base + (size_t)(r & 1) * npairs * PS * PS;
       q.flags = flags_base + (size_t)(r & 1) * npairs;
-      q.stamp = stamp + r + 1;
+      q.stamp = r + 1;
       return q;
     };
-    jac_round<<<npairs, AT, apply_smem, st>>>(round_params(0), round_params(0), 1, 0);
-    count_launches(1);
+    jac_round<<<npairs, AT, apply_smem, ls>>>(round_params(0), round_params(0), 1, 0);
     for (int r = 0; r < R; ++r) {
       Params q = round_params(r);
       q.phase = 1;
-      jac_apply<<<needed_grid, AT, apply_smem, st>>>(q);
-      if (trace > 1 && r == R / 2) cudaEventRecord(ev[0], st);
+      jac_apply<<<needed_grid, AT, apply_smem, ls>>>(q);
+      if (trace > 1 && r == R / 2) cudaEventRecord(ev[0], ls);
       q.phase = 2;
-      jac_round<<<rest_grid, AT, apply_smem, st>>>(q, round_params(r + 1 < R ? r + 1 : 0), r + 1 < R, 1);
-      count_launches(2);
+      jac_round<<<rest_grid, AT, apply_smem, ls>>>(q, round_params(r + 1 < R ? r + 1 : 0), r + 1 < R, 1);
       if (trace > 1 && r == R / 2) {
-        cudaEventRecord(ev[1], st);
-        cudaEventRecord(ev[2], st);
+        cudaEventRecord(ev[1], ls);
+        cudaEventRecord(ev[2], ls);
       }
     }
-    stamp += R;
-    e = d2h_small(host_buf, p.counter, 32, st);  // counter, maxoff, mm_count
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return d2h_small(host_buf, p.counter, 32, ls);  // counter, maxoff, mm_count
+  };
+  struct GraphHolder {
+    cudaGraphExec_t exec = nullptr;
+    ~GraphHolder() {
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+  } graph;
+  bool use_graph = L.np <= GRAPH_MAX_ORDER && trace < 2;
+  cudaStream_t ls = st;
+  if (use_graph) {
+    // the side stream starts after everything queued on st; every sweep ends in a host sync of the
+    // side stream, so the work queued on st afterwards is ordered behind it
+    thread_local cudaStream_t side = nullptr;
+    thread_local cudaEvent_t dep = nullptr;
+    if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) side = nullptr;
+    if (!dep && cudaEventCreateWithFlags(&dep, cudaEventDisableTiming) != cudaSuccess) dep = nullptr;
+    if (side && dep && cudaEventRecord(dep, st) == cudaSuccess && cudaStreamWaitEvent(side, dep, 0) == cudaSuccess)
+      ls = side;
+    else
+      use_graph = false;
+    (void)cudaGetLastError();
+  }
+  for (; sweep < max_sweeps; ++sweep) {
+    cudaError_t e = cudaSuccess;
+    if (use_graph && !graph.exec) {
+      cudaGraph_t g = nullptr;
+      e = cudaStreamBeginCapture(ls, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        const cudaError_t eq = enqueue_sweep(ls);
+        e = cudaStreamEndCapture(ls, &g);
+        if (e == cudaSuccess) e = eq;
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&graph.exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e != cudaSuccess) {  // no capture on this stream / driver: launch directly
+        (void)cudaGetLastError();
+        graph.exec = nullptr;
+        use_graph = false;
+        e = cudaSuccess;
+      }
+    }
+    if (use_graph)
+      e = cudaGraphLaunch(graph.exec, ls);
+    else
+      e = enqueue_sweep(ls);
+    count_launches(2 * R + 4);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
     if (e != cudaSuccess) {
       set_error(std::string("syev sweep: ") + cudaGetErrorString(e));
       return HP_ECUDA;
