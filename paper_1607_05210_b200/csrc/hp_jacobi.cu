@@ -51,6 +51,7 @@ constexpr int LS = PS + 1;    // local smem stride
 constexpr int TS = PS + 4;    // apply-kernel smem stride (= 4 mod 16: conflict-free DMMA fragments)
 constexpr int AT = 256;       // apply threads
 constexpr int64_t GRAPH_MAX_ORDER = 2048;  // padded orders up to this replay their sweeps as CUDA graphs
+constexpr int GRAPH_MIN_CONCURRENCY = 3;   // ... when at least this many solves are in flight on host threads
 
 struct Params {
   double* G;          // n_p x n_p, ld = n_p
@@ -892,14 +893,30 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
       if (exec) cudaGraphExecDestroy(exec);
     }
   } graph;
-  bool use_graph = L.np <= GRAPH_MAX_ORDER && trace < 2;
+  // ... when several host threads are in this routine at once (a leaf wave on stream workers): a
+  // single stream's launches already run ahead of the GPU, and capturing + instantiating a graph per
+  // solve then costs more than it saves (config 2's chain merges: +1.2 ms per merge).
+  static std::atomic<int> active_solves{0};
+  struct ActiveGuard {
+    std::atomic<int>& c;
+    int seen;
+    explicit ActiveGuard(std::atomic<int>& a) : c(a), seen(a.fetch_add(1, std::memory_order_relaxed) + 1) {}
+    ~ActiveGuard() { c.fetch_sub(1, std::memory_order_relaxed); }
+  } guard(active_solves);
+  bool use_graph = L.np <= GRAPH_MAX_ORDER && trace < 2 && guard.seen >= GRAPH_MIN_CONCURRENCY;
   cudaStream_t ls = st;
   if (use_graph) {
     // the side stream starts after everything queued on st; every sweep ends in a host sync of the
     // side stream, so the work queued on st afterwards is ordered behind it
     thread_local cudaStream_t side = nullptr;
     thread_local cudaEvent_t dep = nullptr;
-    if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) side = nullptr;
+    if (!side) {
+      // highest priority: the sweeps are chains of microsecond kernels that would otherwise queue
+      // behind the other leaves' full-chip GEMM tiles
+      int lo_pri = 0, hi_pri = 0;
+      cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+      if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_pri) != cudaSuccess) side = nullptr;
+    }
     if (!dep && cudaEventCreateWithFlags(&dep, cudaEventDisableTiming) != cudaSuccess) dep = nullptr;
     if (side && dep && cudaEventRecord(dep, st) == cudaSuccess && cudaStreamWaitEvent(side, dep, 0) == cudaSuccess)
       ls = side;
