@@ -60,15 +60,36 @@ def _case(rng):
     return tree, maps, d, cols, data, w, counts, eps, total
 
 
-def test_random_trees_budget_mode_bound_and_oracle_counts():
+@pytest.mark.parametrize("tri_min_order,cases", [(None, CASES), (4, 80)])
+def test_random_trees_budget_mode_bound_and_oracle_counts(tri_min_order, cases):
+    """tri_min_order = 4 sends EVERY preconditioned eigenproblem of order >= 4 through the tridiagonal
+    solver (hp_syev_tri; production uses it from order 1,024 up), including the spectra it has to
+    decline -- exact zeros, repeated singular values -- which must fall back to block Jacobi."""
+    from paper_1607_05210_b200 import _device as D
+    saved = D.TRI_MIN_ORDER
+    if tri_min_order is not None:
+        D.TRI_MIN_ORDER = tri_min_order
+    try:
+        _run_cases(cases, D if tri_min_order is not None else None)
+    finally:
+        D.TRI_MIN_ORDER = saved
+
+
+def _run_cases(ncases, D):
     rng = np.random.default_rng(SEED)
     nodes_checked, worst = 0, 0.0
-    for case in range(CASES):
+    tri_done = tri_declined = 0
+    for case in range(ncases):
         tree, maps, d, cols, data, w, counts, eps, total = _case(rng)
         sp = H.InnerProductSpace(d, w)
         la = H.distribute_columns(tree, H.SnapshotBlock(sp, data), counts=counts)
         tol = H.ToleranceAssignment(tuple(float(e) for e in eps))
+        if D is not None:
+            D.LAST_TRI_DIAG.clear()
         res = H.run_hapod(tree, la, tol)
+        if D is not None and D.LAST_TRI_DIAG:
+            tri_done += D.LAST_TRI_DIAG["status"] == 0
+            tri_declined += D.LAST_TRI_DIAG["status"] != 0
         blocks = {leaf: np.asarray(la.blocks[leaf].values) for leaf in maps.leaf_order}
         ref = O.run_hapod([list(c) for c in tree.children], 0, blocks, list(tol.epsilons), weights=w)
         # every node's output count equals the oracle's
@@ -92,5 +113,8 @@ def test_random_trees_budget_mode_bound_and_oracle_counts():
             floor = 2.2e-16 * (s[0] / s) ** 2
             rel = np.abs(np.asarray(res.modes.sigmas) - s) / s
             assert np.all(rel <= np.maximum(1e-9, 1e3 * floor)), (case, rel.max())
-    print(f"\n[acceptance] {CASES} random trees, {nodes_checked} node outputs: counts equal to the oracle's, "
-          f"within flat-POD counts and within budget (worst overshoot {worst:.3e})")
+    print(f"\n[acceptance] {ncases} random trees, {nodes_checked} node outputs: counts equal to the oracle's, "
+          f"within flat-POD counts and within budget (worst overshoot {worst:.3e})"
+          + (f"; last tridiagonal solve per tree: {tri_done} completed, {tri_declined} declined" if D is not None else ""))
+    if D is not None:
+        assert tri_done > ncases // 2  # the forced path really ran

@@ -339,3 +339,45 @@ def test_space_gram_rejects_mismatched_rows():
     sp = H.InnerProductSpace(10)
     with pytest.raises(ValueError):
         sp.gram(np.ones((10, 2)), np.ones((11, 2)))
+
+
+def test_tridiagonal_path_at_pod_level_and_its_fallback():
+    """pod() with the tridiagonal H-phase solver forced on small nodes (production threshold: order
+    1,024): same counts / sigma / span as the oracle (pod.py:296-348); a block with two repeated
+    singular values makes the solver decline and the block Jacobi take over."""
+    from paper_1607_05210_b200 import _device as D
+    rng = np.random.default_rng(11)
+    d, m = 3000, 400
+    q1, _ = np.linalg.qr(rng.standard_normal((d, m)))
+    q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    vals = (q1 * 10.0 ** (-7.0 * np.arange(m) / (m - 1))) @ q2.T
+    saved = D.TRI_MIN_ORDER
+    try:
+        D.TRI_MIN_ORDER = 8
+        D.LAST_TRI_DIAG.clear()
+        eps = 1e-5 * float(np.linalg.norm(vals))
+        out = H.pod(H.SnapshotBlock(euclid(d), vals), eps)
+        assert D.LAST_TRI_DIAG.get("status") == 0 and D.LAST_TRI_DIAG["count"] > 100
+        ref = O.pod(vals, eps)
+        assert out.count == ref.count
+        # method-of-snapshots floor of a singular value: u * (sigma_1 / sigma_i)^2 (cf. the MGS golden test)
+        floor = 2.2e-16 * (ref.sigmas[0] / ref.sigmas) ** 2
+        assert np.all(np.abs(out.sigmas - ref.sigmas) / ref.sigmas <= np.maximum(1e-10, 10 * floor))
+        assert angles(out.modes, ref.modes).max() < 1e-6
+        # one repeated singular value: the shift next to it resolves the cluster (MRRR's own device)
+        D.LAST_TRI_DIAG.clear()
+        out = H.pod(H.SnapshotBlock(euclid(d), q1[:, :200]), 0.5)
+        assert out.count == 200 and np.allclose(out.sigmas, 1.0, rtol=1e-12)
+        # two repeated singular values: the cluster away from the shift has no relative gaps left,
+        # the solver declines (status 1) and the block Jacobi takes over
+        D.LAST_TRI_DIAG.clear()
+        two = np.hstack([2.0 * q1[:, :100], q1[:, 100:200]])
+        out = H.pod(H.SnapshotBlock(euclid(d), two), 0.5)
+        assert D.LAST_TRI_DIAG.get("status") == 1
+        ref = O.pod(two, 0.5)
+        assert out.count == ref.count == 200
+        assert np.allclose(out.sigmas, ref.sigmas, rtol=1e-12)
+        g = out.modes.T @ out.modes
+        assert np.max(np.abs(g - np.eye(200))) < 1e-10
+    finally:
+        D.TRI_MIN_ORDER = saved
