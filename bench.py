@@ -19,6 +19,10 @@ e2e    : the same through the public API from pinned HOST memory: each step
 roofline: the dominant kernel family by device time inside the timed region
          (CUDA events on the launching stream), its algorithmic FP64 flops
           / its time, against the measured FP64 DMMA peak.
+         ``roofline.eigensolver``: the HBM-bound side of the step -- the tridiagonalisation
+         kernel (sytrd_panel) of the root's eigensolve, its algorithmic matrix reads
+         (8 r^3 / 3 bytes, reported by hp_syev_tri with its own CUDA-event time) against
+         MEASURED_PEAKS.json's copy bandwidth -- and the polish Jacobi's DMMA rate.
 cpu_baseline / --impl reference: the reference algorithm (the oracle port of hapod,
          NumPy + SciPy + OpenBLAS with all host threads; data from oracle/hostgen.py -- no
          product code, no CUDA) over the WHOLE tree of the config (all leaves + the root,

@@ -542,42 +542,47 @@ __global__ void __launch_bounds__(512, 1) tri_prepare(const double* a, const dou
   }
 }
 
-// One warp per wanted eigenvalue (descending index k): 32-way multisection on a geometric grid (small
+// Eight lanes per wanted eigenvalue (descending index k; a full warp per eigenvalue was bound by the
+// SM's issue slots: 37 warps per SM of division chains): 9-way multisection on a geometric grid (small
 // eigenvalues are located to the same RELATIVE accuracy as large ones) until the bracket holds
 // exactly this eigenvalue and is narrower than 2^-30 octaves; tri_getvec's Rayleigh-quotient
-// iteration converges in one step from there.  A cluster keeps subdividing (at most 14 rounds).
+// iteration converges in one step from there.  A cluster keeps subdividing (at most 24 rounds).
+constexpr int BL = 8;  // lanes per eigenvalue in tri_bisect
 __global__ void __launch_bounds__(256) tri_bisect(const double* d, const double* lld, int n, int K, const double* info,
                                                   double* lam_s, double* blo, double* bhi) {
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) / BL;
   const int lane = threadIdx.x & 31;
+  const int sub = lane & (BL - 1);
+  const int gbase = lane & ~(BL - 1);
+  const unsigned gmask = ((1u << BL) - 1u) << gbase;  // this eigenvalue's lanes (groups diverge freely)
   if (k >= K) return;
   const int want = n - 1 - k;
   const double pivmin = info[I_PIVMIN];
   double lo = info[I_LO], hi = info[I_HI];
   int clo = 0, chi = n;  // eigenvalues below lo / below hi
-  for (int round = 0; round < 14; ++round) {
+  for (int round = 0; round < 24; ++round) {
     const double lr = log2(hi / lo);
     if (!(lr > 8.0 * UNIT)) break;
     if (clo == want && chi == want + 1 && lr <= 0x1p-30) break;
-    double xq = lo * exp2(lr * (double)(lane + 1) / 33.0);
+    double xq = lo * exp2(lr * (double)(sub + 1) / (double)(BL + 1));
     xq = fmin(fmax(xq, lo), hi);
     const int c = negcount(d, lld, n, xq, pivmin);
-    const unsigned okm = __ballot_sync(FULL, c <= want);
+    const unsigned okm = (__ballot_sync(gmask, c <= want) & gmask) >> gbase;
     const int cnt = __popc(okm);
-    const double nlo = __shfl_sync(FULL, xq, max(cnt - 1, 0));
-    const int nclo = __shfl_sync(FULL, c, max(cnt - 1, 0));
-    const double nhi = __shfl_sync(FULL, xq, min(cnt, 31));
-    const int nchi = __shfl_sync(FULL, c, min(cnt, 31));
+    const double nlo = __shfl_sync(gmask, xq, gbase + max(cnt - 1, 0));
+    const int nclo = __shfl_sync(gmask, c, gbase + max(cnt - 1, 0));
+    const double nhi = __shfl_sync(gmask, xq, gbase + min(cnt, BL - 1));
+    const int nchi = __shfl_sync(gmask, c, gbase + min(cnt, BL - 1));
     if (cnt > 0) {
       lo = nlo;
       clo = nclo;
     }
-    if (cnt < 32) {
+    if (cnt < BL) {
       hi = nhi;
       chi = nchi;
     }
   }
-  if (lane == 0) {
+  if (sub == 0) {
     lam_s[k] = sqrt(lo) * sqrt(hi);
     blo[k] = lo;
     bhi[k] = hi;
@@ -1007,7 +1012,7 @@ int syev_tri_run(const double* H, int64_t ldh, int64_t n64, double floor_rel, do
     *status_out = 0;
     return HP_OK;
   }
-  tri_bisect<<<(unsigned)ceil_div((int64_t)K * 32, 256), 256, 0, st>>>(d1, lld1, n, K, info, lam_s, blo, bhi);
+  tri_bisect<<<(unsigned)ceil_div((int64_t)K * BL, 256), 256, 0, st>>>(d1, lld1, n, K, info, lam_s, blo, bhi);
   HP_CHECK_LAUNCH("tri_bisect");
   tri_getvec<<<(unsigned)ceil_div(K, 32), 32, 0, st>>>(d1, l1, ld1, lld1, n, K, lda, info, lam_s, blo, bhi, LP, UM,
                                                          PP, W, ldw, lam_desc, resid, reinterpret_cast<int*>(vec[16]));

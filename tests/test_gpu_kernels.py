@@ -379,3 +379,9 @@ def test_syev_tri_declines_clusters():
     assert status == 1
     status, *_ = _tri_solve(np.eye(n), 1e-12)
     assert status == 1
+
+
+def test_syev_tri_order_4200():
+    """A root-sized order (trailing matrix larger than the L2 at the start): eigenvalues, residuals
+    and orthogonality as for the small orders."""
+    test_syev_tri_graded_spectrum_vs_eigh(4200, 11)
