@@ -652,9 +652,12 @@ def _syev_tri(H: DevMat, r: int, floor_rel: float, st):
     lib = N.load()
     if r < 2 or r > int(lib.hp_syev_tri_max_order()):
         return None
-    lam = torch.empty(r, dtype=torch.float64, device="cuda")
-    W = DevMat.empty(r, r)
-    ws = _ws(lib.hp_syev_tri_workspace_bytes(r))
+    try:
+        lam = torch.empty(r, dtype=torch.float64, device="cuda")
+        W = DevMat.empty(r, r)
+        ws = _ws(lib.hp_syev_tri_workspace_bytes(r))  # ~6 r^2 doubles: reflectors, qds factors per eigenvalue
+    except torch.cuda.OutOfMemoryError:
+        return None  # the block Jacobi needs ~3 r^2 doubles
     k = ctypes.c_int64(0)
     status = ctypes.c_int(1)
     diag = (ctypes.c_double * 8)()
