@@ -788,7 +788,7 @@ def bench_resident(a, world, rank, local, torch, dist, H, D, DI, W, lib):
     e2e = {"value": round(e2e_cols, 3), "unit": "cols/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": 8 * (res_modes or 0),
            "modes_d2h_bytes_if_requested": 8 * d * (res_modes or 0),
-           "note": "sigmas read back; the final ModeSet stays device-resident (SURVEY.md 8d)"}
+           "note": "sigmas read back; the final ModeSet stays device-resident (SURVEY.md 8d); under the upload-bound leaf wave run_parallel accumulates the root Gramian child pair by child pair (bit-identical to the monolithic launch)"}
     return base_line(a, world, cols_per_s, step_ms, "strong",
                      "synthetic (seeded on device, BASELINE config generator; no dataset involved)", par, e2e,
                      launches, roofline, cpu, clk,

@@ -77,6 +77,21 @@ size_t hp_gram_workspace_bytes(int64_t d, int64_t m);
 int hp_gram(hp_vecset S, int64_t d, int64_t m, const double* colscale, double* G, int64_t ldg, void* ws,
             size_t ws_bytes, void* stream);
 
+/* K1, one child pair at a time (a star's root under run_parallel, parallel.py:77-142 evaluates the
+ * parent only after the whole wave; the Gramian of hstack(children) at hierarchy.py:284-291 +
+ * pod.py:208-211 can start as soon as two children exist): G (na x nb) = diag(sa) Ua^T Ub diag(sb)
+ * with the tile arithmetic of an UNSPLIT hp_gram -- every output entry summed over all d rows by one
+ * CTA -- so that the block equals the corresponding block of hp_gram on the concatenation bit for bit
+ * whenever hp_gram_single_split(m, d) != 0 for the concatenation's order m.  same != 0: Ua == Ub
+ * (diagonal block, exactly symmetric).  hp_gram forms the entries with row <= column and mirrors them
+ * (row scale applied before the column scale), so an off-diagonal pair is computed as the UPPER
+ * block -- rows = the child that comes first -- and hp_mirror_upper copies the strictly upper
+ * triangle of the assembled n x n matrix onto the lower one. */
+int hp_gram_single_split(int64_t m, int64_t d);
+int hp_gram_pair(hp_vecset Ua, const double* sa, int64_t na, hp_vecset Ub, const double* sb, int64_t nb, int64_t d,
+                 int same, double* G, int64_t ldg, void* stream);
+int hp_mirror_upper(double* G, int64_t ldg, int64_t n, void* stream);
+
 /* K1b -- block Gramian of [Phi*diag(sigma) | F*diag(fscale)] for the
  * incremental merge (pod.py:376-384): top-left diag(sigma^2) written down,
  * mixed block sigma o (Phi^T F), fresh block F^T F, exactly symmetric.

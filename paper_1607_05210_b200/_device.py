@@ -50,6 +50,8 @@ POLISH_TOL_ABS = 1e-30
 POLISH_TOL_ANGLE = 1e-14
 # absolute trigger of the preconditioned (H = L^T L) phase; the polish carries the final accuracy
 PC_TOL_ABS = 16 * 2.0 ** -52
+# run_parallel accumulates a star root's Gramian pair by pair beside an upload-bound wave of leaves
+PROGRESSIVE_GRAM = True
 # Preconditioned eigenproblems of at least this order go through the tridiagonal solver
 # (hp_syev_tri: ~4/3 r^3 flops instead of the block Jacobi's ~90 r^3); it declines clustered
 # spectra (a relative gap below TRI_RELGAP_MIN), which then take the Jacobi path.
@@ -916,14 +918,159 @@ def spectrum_and_modes(G: DevMat, m: int, parts: list[Part], d: int, eps: float,
     return NodeOutput(U, sig_host, sig_dev, float(tail), R, lam_max, nkeep, drift, reorthed, sweeps, m)
 
 
-def node_pod(parts: list[Part], d: int, eps: float, cutoff: float, want_right: bool, sqrt_w=None) -> NodeOutput:
-    """Full device pod() of the concatenated parts (pod.py:328-337)."""
+def node_pod(parts: list[Part], d: int, eps: float, cutoff: float, want_right: bool, sqrt_w=None,
+             gram: "DevMat | None" = None) -> NodeOutput:
+    """Full device pod() of the concatenated parts (pod.py:328-337).  ``gram``: the Gramian of the
+    (scaled) concatenation when the caller already has it (ProgressiveGram), bit-identical to gram_full's."""
     if sqrt_w is not None:
         parts = weigh_parts(parts, sqrt_w)
+        gram = None
     with _phase("pack"):
         parts = pack_parts(parts)
-    G, m, _keep = gram_full(parts, d)
+    m = sum(p.mat.cols for p in parts)
+    if gram is not None and gram.rows == m and gram.cols == m and m > 0:
+        G = gram
+    else:
+        G, m, _keep = gram_full(parts, d)
     return spectrum_and_modes(G, m, parts, d, eps, cutoff, want_right, sqrt_w)
+
+
+class ProgressiveGram:
+    """The Gramian of a star root's input, hstack(children's sigma-scaled modes) (hierarchy.py:284-291 +
+    pod.py:208-211), accumulated child pair by child pair on background streams while later children
+    are still being evaluated -- the reference's wave executor (parallel.py:77-142) starts the parent
+    only after the whole wave.  Every pair block is an hp_gram_pair (unsplit contraction), so the
+    assembled matrix equals hp_gram on the packed concatenation bit for bit as long as that launch is
+    unsplit too (hp_gram_single_split); otherwise finish() returns None and the parent computes its
+    Gramian as usual.  Used by run_parallel when a wave of leaves is bound by its host-to-device
+    copies (deferred uploads), where the GPU would otherwise idle.
+
+    At most WAVE_INFLIGHT pair GEMMs (16 CTAs each, one 128 x 128 tile over the whole contraction per
+    CTA) run beside the wave, none once only TAIL_CHILDREN children are outstanding; finish() releases
+    the rest on DRAIN_STREAMS streams."""
+
+    WAVE_INFLIGHT = 8    # measured (tools/e2e_progressive_probe.py): 3..8 in flight all land within 2 % of each other
+    TAIL_CHILDREN = 4
+    TAIL_INFLIGHT = 0
+    DRAIN_STREAMS = 10
+    _streams: list = []
+    _lock = threading.Lock()
+
+    def __init__(self, d: int, children: list[int], slot_cols: list[int]):
+        self.d = int(d)
+        self.children = list(children)
+        self.pos = {c: i for i, c in enumerate(self.children)}
+        self.slot, self.width, off = {}, {}, 0
+        for c, n in zip(self.children, slot_cols):
+            self.slot[c] = off
+            self.width[c] = int(n)
+            off += _even(int(n))
+        self.m_up = off
+        self.G = DevMat.empty(off, off, zero=True)
+        self.parts: dict = {}      # child -> Part (U, sigma) or None for an empty child
+        self.queue: list = []      # pending (row child, column child): upper blocks, rows = the earlier child
+        self.events: list = []     # events of launched pairs
+        self.ok = True
+        main = torch.cuda.current_stream()
+        with ProgressiveGram._lock:
+            if not ProgressiveGram._streams:  # default (lowest) priority: the stream workers run above it
+                ProgressiveGram._streams = [torch.cuda.Stream() for _ in range(self.DRAIN_STREAMS)]
+        self.streams = ProgressiveGram._streams
+        for s in self.streams:
+            s.wait_stream(main)    # the zero fill of G
+        self.turn = 0
+
+    def add(self, child: int, modes) -> None:
+        """Child ``child`` finished with ModeSet ``modes`` (its stream is idle: evaluate_node ends with a
+        device synchronize).  Queues its pairs with every finished sibling and launches what fits."""
+        if not self.ok:
+            return
+        try:
+            parts = modes.scaled_parts() if modes.count else []
+            if modes.count and (len(parts) != 1 or parts[0].scale is None or not modes.orthonormal
+                                or not parts[0].mat.aligned16()
+                                or parts[0].mat.cols > self.width[child]):
+                self.ok = False
+                return
+            self.parts[child] = parts[0] if modes.count else None
+            if modes.count:
+                for other, q in self.parts.items():
+                    if q is None or other == child:
+                        continue
+                    # hp_gram forms the entries with row <= column: rows = the earlier child
+                    pair = (child, other) if self.pos[child] < self.pos[other] else (other, child)
+                    self.queue.append(pair)
+                self.queue.append((child, child))
+            # the background work pays while the wave waits for uploads; once only TAIL_CHILDREN children
+            # are outstanding the wave is compute-bound and gets the GPU to itself until finish()
+            outstanding = len(self.children) - len(self.parts)
+            self._pump(self.WAVE_INFLIGHT if outstanding > self.TAIL_CHILDREN else self.TAIL_INFLIGHT)
+        except Exception:
+            self.ok = False
+
+    def _pump(self, limit: int) -> None:
+        self.events = [e for e in self.events if not e.query()]
+        lib = N.load()
+        while self.queue and len(self.events) < limit:
+            a, b = self.queue.pop(0)
+            pa, pb = self.parts[a], self.parts[b]
+            s = self.streams[self.turn % len(self.streams)]
+            self.turn += 1
+            dst = self.G.ptr + 8 * (self.slot[a] + self.slot[b] * self.G.ld)
+            N.check(lib.hp_gram_pair(pa.mat.vecset(), pa.scale.data_ptr(), pa.mat.cols, pb.mat.vecset(),
+                                     pb.scale.data_ptr(), pb.mat.cols, self.d, int(a == b), dst, self.G.ld,
+                                     s.cuda_stream), "Gram pair")
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self.events.append(ev)
+
+    def finish(self):
+        """Launch what is still queued, make the caller's stream wait for all of it and return the
+        Gramian of the compact concatenation (children in list order), or None when the result
+        would not be bit-identical to gram_full's."""
+        lib = N.load()
+        try:
+            if not self.ok or set(self.parts) != set(self.children):
+                return None
+            live = [c for c in self.children if self.parts[c] is not None]
+            m = sum(self.parts[c].mat.cols for c in live)
+            if len(live) < PACK_MIN_PARTS or not lib.hp_gram_single_split(m, self.d):
+                return None
+            self._pump(1 << 30)
+            main = torch.cuda.current_stream()
+            for s in self.streams:
+                main.wait_stream(s)
+            st = _stream()
+            G = self.G
+            off, at = {}, 0
+            for c in live:
+                off[c] = at
+                at += self.parts[c].mat.cols
+            if any(off[c] != self.slot[c] for c in live):  # children kept fewer modes than their slots: compact
+                G = DevMat.empty(m, m)
+                for a in live:
+                    for b in live:
+                        if self.pos[a] > self.pos[b]:
+                            continue
+                        na, nb = self.parts[a].mat.cols, self.parts[b].mat.cols
+                        src = self.G.ptr + 8 * (self.slot[a] + self.slot[b] * self.G.ld)
+                        dst = G.ptr + 8 * (off[a] + off[b] * G.ld)
+                        N.check(lib.hp_scale(src, self.G.ld, na, nb, None, None, None, dst, G.ld, st), "compact Gram")
+            elif m != self.m_up:
+                G = self.G.view_cols(0, m)
+                G = DevMat(G.storage, m, m, G.ld, G.offset)
+            N.check(lib.hp_mirror_upper(G.ptr, G.ld, m, st), "mirror Gram")
+            return G
+        except Exception:
+            return None
+        finally:
+            self.wait()
+
+    def wait(self) -> None:
+        """Nothing of this object may still run once the children's matrices are released."""
+        self.queue.clear()
+        for s in self.streams:
+            torch.cuda.current_stream().wait_stream(s)
 
 
 def node_block_pod(prior_U: DevMat, prior_sig_dev, fresh: list[Part], d: int, eps: float, cutoff: float,

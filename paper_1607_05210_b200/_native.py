@@ -40,6 +40,9 @@ _SIGNATURES = {
                         c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_size, c_vp]),
     "hp_gram_workspace_bytes": (c_size, [c_i64, c_i64]),
     "hp_gram": (c_int, [VecSet, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_size, c_vp]),
+    "hp_gram_single_split": (c_int, [c_i64, c_i64]),
+    "hp_gram_pair": (c_int, [VecSet, c_vp, c_i64, VecSet, c_vp, c_i64, c_i64, c_int, c_vp, c_i64, c_vp]),
+    "hp_mirror_upper": (c_int, [c_vp, c_i64, c_i64, c_vp]),
     "hp_block_gram_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "hp_block_gram": (c_int, [VecSet, c_vp, c_i64, VecSet, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_size, c_vp]),
     "hp_pstrf_workspace_bytes": (c_size, [c_i64]),

@@ -37,6 +37,8 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
              double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
              const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
+void gemm_set_nosplit(bool on);
+bool gemm_plan_is_single_split(int64_t M, int64_t N, int64_t K, int sym);
 size_t syev_workspace_bytes(int64_t n);
 int64_t syev_padded_order(int64_t n);
 int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* V, int64_t ldv, int64_t nvec,
@@ -204,6 +206,34 @@ int hp_gram(hp_vecset S, int64_t d, int64_t m, const double* colscale, double* G
   HP_REQUIRE(d >= 0 && m >= 0 && ldg >= m, "hp_gram: bad dimensions");
   return gemm_run(true, true, m, m, d, vs(S), vs(S), S.aligned16 != 0, 1.0, 0.0, G, ldg, colscale, colscale, nullptr,
                   1, 0, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int hp_gram_single_split(int64_t m, int64_t d) { return gemm_plan_is_single_split(m, m, d, 1) ? 1 : 0; }
+
+int hp_gram_pair(hp_vecset Ua, const double* sa, int64_t na, hp_vecset Ub, const double* sb, int64_t nb, int64_t d,
+                 int same, double* G, int64_t ldg, void* stream) {
+  HP_REQUIRE(na >= 0 && nb >= 0 && d >= 0 && ldg >= na && G, "hp_gram_pair: bad dimensions");
+  HP_REQUIRE(!same || na == nb, "hp_gram_pair: a diagonal block is square");
+  gemm_set_nosplit(true);
+  const int rc = gemm_run(true, true, na, nb, d, vs(Ua), vs(Ub), Ua.aligned16 && Ub.aligned16, 1.0, 0.0, G, ldg, sa, sb,
+                          nullptr, same ? 1 : 0, 0, nullptr, 0, (cudaStream_t)stream);
+  gemm_set_nosplit(false);
+  return rc;
+}
+
+__global__ void mirror_upper_kernel(double* G, int64_t ldg, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int64_t i = e % n, j = e / n;
+  if (i > j) G[i + j * ldg] = G[j + i * ldg];
+}
+
+int hp_mirror_upper(double* G, int64_t ldg, int64_t n, void* stream) {
+  HP_REQUIRE(n >= 0 && ldg >= std::max<int64_t>(n, 1), "hp_mirror_upper: bad dimensions");
+  if (n == 0) return HP_OK;
+  mirror_upper_kernel<<<(unsigned)ceil_div(n * n, 256), 256, 0, (cudaStream_t)stream>>>(G, ldg, n);
+  HP_CHECK_LAUNCH("mirror_upper_kernel");
+  return HP_OK;
 }
 
 size_t hp_block_gram_workspace_bytes(int64_t d, int64_t n_old, int64_t m) {

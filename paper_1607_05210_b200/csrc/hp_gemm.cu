@@ -635,6 +635,16 @@ int launch_tma(const Params& p, cudaStream_t st, bool& done) {
 
 }  // namespace gemm
 
+// Calling-thread switch for the next gemm_run calls: never split the contraction and keep the 128-wide
+// tiles, whatever the output size -- every output entry is then summed over all K by one CTA in the
+// order of a large (unsplit) launch, so a block of a big Gramian computed on its own equals the
+// corresponding block of the monolithic launch bit for bit (hp_gram_pair).
+static thread_local bool tl_nosplit = false;
+void gemm_set_nosplit(bool on) { tl_nosplit = on; }
+bool gemm_plan_is_single_split(int64_t M, int64_t N, int64_t K, int sym) {
+  return gemm::make_plan(M, N, K, sym, 0).splits == 1;
+}
+
 // Host entry used by the C-ABI and by the other modules.
 int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecSet A, VecSet B, bool aligned16,
              double alpha, double beta, double* C, int64_t ldc, const double* row_scale, const double* col_scale,
@@ -678,8 +688,13 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   };
   const bool tma_ok = aligned16 && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31);
   // narrow n tiles (96 / 64 wide) exist on the TMA path with a K-major B operand only
-  const int bn = (tma_ok && b_kmajor && !sym && !b_upper) ? narrow_bn(N) : BN;
+  const int bn = (tma_ok && b_kmajor && !sym && !b_upper && !tl_nosplit) ? narrow_bn(N) : BN;
   apply_plan(make_plan(M, N, K, sym, b_upper, bn));
+  if (tl_nosplit) {
+    p.splits = 1;
+    p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
+    p.partial = nullptr;
+  }
   int rc = HP_OK;
   bool done = false;
   if (tma_ok) {

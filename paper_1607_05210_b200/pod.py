@@ -439,9 +439,10 @@ def _from_node_output(space, out: "D.NodeOutput", want_right) -> ModeSet:
                            right=out.right if want_right else None, sig_dev=out.sigmas_dev, diagnostics=diag)
 
 
-def pod_parts(space, parts, epsilon: float, backend=None, want_right: bool = False) -> ModeSet:
+def pod_parts(space, parts, epsilon: float, backend=None, want_right: bool = False, gram=None) -> ModeSet:
     """pod() of the concatenation of device parts (used by the tree drivers:
-    interior nodes pass their children's scaled parts, no hstack copy)."""
+    interior nodes pass their children's scaled parts, no hstack copy).  ``gram``: the
+    concatenation's Gramian when the driver already accumulated it (D.ProgressiveGram)."""
     if epsilon < 0.0:
         raise ValueError("epsilon must be nonnegative")
     backend = _check_backend(backend)
@@ -452,7 +453,7 @@ def pod_parts(space, parts, epsilon: float, backend=None, want_right: bool = Fal
     if m == 0:
         return _empty(space, want_right)
     out = D.node_pod(parts, space.dimension, epsilon, backend.gram_eig_cutoff_factor, want_right,
-                     space.sqrt_weights_device())
+                     space.sqrt_weights_device(), gram=gram)
     return _from_node_output(space, out, want_right)
 
 
