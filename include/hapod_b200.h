@@ -51,7 +51,8 @@ int hp_abi_version(void);
 long long hp_launch_count(void);
 /* Diagnostics (no reference counterpart; never changes a result): bit 0 prints one line per
  * Jacobi sweep, bit 1 adds CUDA-event timing of one mid-sweep round, bit 2 times the CholQR
- * factorisation, bit 3 times the stages of hp_syev_tri.  Returns the previous flags.  The library reads no environment variables. */
+ * factorisation, bit 3 times the stages of hp_syev_tri, bit 4
+ * launches the Jacobi sweeps directly instead of replaying CUDA graphs (for per-kernel profilers).  Returns the previous flags.  The library reads no environment variables. */
 int hp_set_debug(int flags);
 const char* hp_last_error(void);
 int hp_device_sm_count(int device);

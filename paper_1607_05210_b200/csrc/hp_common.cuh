@@ -134,7 +134,7 @@ int num_sms();
 
 // Diagnostics switched on through the C-ABI (hp_set_debug), never through the environment:
 // they only add CUDA-event timing printouts and never change a result.
-enum DebugFlags { DBG_JACOBI_TRACE = 1, DBG_JACOBI_ROUND_TIMING = 2, DBG_CHOL_TRACE = 4, DBG_TRI_TRACE = 8 };
+enum DebugFlags { DBG_JACOBI_TRACE = 1, DBG_JACOBI_ROUND_TIMING = 2, DBG_CHOL_TRACE = 4, DBG_TRI_TRACE = 8, DBG_NO_GRAPHS = 16 };
 int debug_flags();
 
 // One-time per-DEVICE setup of kernel attributes (cudaFuncSetAttribute applies to the current

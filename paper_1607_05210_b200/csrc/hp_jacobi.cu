@@ -903,7 +903,7 @@ int syev_run(const double* G, int64_t ldg, int64_t n, double* lam_desc, double* 
     explicit ActiveGuard(std::atomic<int>& a) : c(a), seen(a.fetch_add(1, std::memory_order_relaxed) + 1) {}
     ~ActiveGuard() { c.fetch_sub(1, std::memory_order_relaxed); }
   } guard(active_solves);
-  bool use_graph = L.np <= GRAPH_MAX_ORDER && trace < 2 && guard.seen >= GRAPH_MIN_CONCURRENCY;
+  bool use_graph = L.np <= GRAPH_MAX_ORDER && trace < 2 && guard.seen >= GRAPH_MIN_CONCURRENCY && !(dbg & DBG_NO_GRAPHS);
   cudaStream_t ls = st;
   if (use_graph) {
     // the side stream starts after everything queued on st; every sweep ends in a host sync of the
