@@ -92,6 +92,11 @@ class NativeMissing(RuntimeError):
     pass
 
 
+# set in the target process by Nsight Compute / Nsight Systems / CUPTI-injection tools
+_PROFILER_ENV = ("CUDA_INJECTION64_PATH", "NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NV_NSIGHT_INJECTION_PORT_BASE",
+                 "NSYS_PROFILING_SESSION_ID")
+
+
 def load(path: str | None = None):
     """Load (once) and return the ctypes handle; raises if the .so is absent."""
     global _lib
@@ -112,6 +117,10 @@ def load(path: str | None = None):
             fn.argtypes = args
         if lib.hp_abi_version() != ABI_VERSION:
             raise NativeMissing(f"ABI mismatch: library {lib.hp_abi_version()} != {ABI_VERSION}")
+        if any(v in os.environ for v in _PROFILER_ENV):
+            # under an injected per-kernel profiler (ncu crashed on replayed graph launches): launch the
+            # Jacobi sweeps directly -- a launch mechanism only, no result depends on it
+            lib.hp_set_debug(lib.hp_set_debug(0) | 16)
         _lib = lib
         return lib
 
