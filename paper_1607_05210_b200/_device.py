@@ -52,10 +52,15 @@ POLISH_TOL_ANGLE = 1e-14
 PC_TOL_ABS = 16 * 2.0 ** -52
 # run_parallel accumulates a star root's Gramian pair by pair beside an upload-bound wave of leaves
 PROGRESSIVE_GRAM = True
+# ... and also beside a wave of device-resident leaves (their latency-bound phases leave SMs idle)
+PROGRESSIVE_GRAM_RESIDENT = False
 # Preconditioned eigenproblems of at least this order go through the tridiagonal solver
 # (hp_syev_tri: ~4/3 r^3 flops instead of the block Jacobi's ~90 r^3); it declines clustered
-# spectra (a relative gap below TRI_RELGAP_MIN), which then take the Jacobi path.
-TRI_MIN_ORDER = 1024
+# spectra (a relative gap below TRI_RELGAP_MIN), which then take the Jacobi path.  Measured
+# (tools/tri_order_probe.py): at order 1,000 (config 0) the H phase takes 14 ms against the block
+# Jacobi's 26 ms; at order 512 a LONE solve would also win, but sytrd_panel is a cooperative launch
+# over every SM, so 16 concurrent leaf solves serialise (config-1 leaf wave 158 -> 231 ms).
+TRI_MIN_ORDER = 896
 TRI_RELGAP_MIN = 1e-9
 LAST_TRI_DIAG: dict = {}
 
