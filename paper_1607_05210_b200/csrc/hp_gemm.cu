@@ -25,6 +25,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -75,7 +79,24 @@ struct Layout {
 constexpr int GN = 8;
 
 __device__ __forceinline__ void tile_coords(const Params& p, int64_t t, int& bi, int& bj) {
-  if (p.sym) {
+  if (p.sym && p.tiles_m <= GN) {
+    // one super-column: the off-diagonal tiles row by row, then the diagonal tiles (which cost about
+    // half a tile on the TMA path, mma_ktile_diag) -- the order make_plan's makespan model assumes
+    const int T = p.tiles_m;
+    const int64_t off = (int64_t)T * (T - 1) / 2;
+    if (t >= off) {
+      bi = bj = (int)(t - off);
+    } else {
+      int64_t r = t;
+      int i = 0;
+      while (r >= T - 1 - i) {
+        r -= T - 1 - i;
+        ++i;
+      }
+      bi = i;
+      bj = i + 1 + (int)r;
+    }
+  } else if (p.sym) {
     // upper triangle (bi <= bj) in super-columns of GN tile columns: group g holds columns
     // [g GN, g GN + gn), first the full rows bi < g GN (gn tiles each), then the triangle
     const int T = p.tiles_m;
@@ -402,6 +423,101 @@ __device__ __forceinline__ void mma_ktile_sw(const char* as, const char* bs, dou
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Diagonal tile of a symmetric product (both operands K-major, 128-wide tile): only the entries
+// with row <= column are wanted, i.e. 136 of the tile's 256 8x8 accumulator fragments.  The
+// regular 2 x 4 warp grid would leave two warps idle and six at full load, so the fragments are
+// re-dealt: the tile is cut into strips of 16 columns; a strip of the full upper-right 64 x 64
+// block takes 8 row fragments, strip s of a diagonal 64 x 64 block 2 (s + 1).  Every consumer
+// warp gets up to two strips (18 +- 2 fragments of 8 x 16) such that the two warps sharing an
+// SM sub-partition (w, w + 4) carry 36 fragments together instead of 64: the tile costs ~56 % of
+// a full one.  Each output entry is still one accumulator summed over k in the same order, so
+// the result equals the regular path's bit for bit.
+struct DiagTask {
+  int rb[2], lim[2], cb[2];  // per strip: first row, row fragments (0 = none), first column
+};
+
+__device__ __forceinline__ DiagTask diag_task(int warp) {
+  DiagTask k;
+  k.rb[1] = 0;
+  k.lim[1] = 0;
+  k.cb[1] = 0;
+  switch (warp) {
+    case 0: k.rb[0] = 0, k.lim[0] = 8, k.cb[0] = 64, k.rb[1] = 0, k.lim[1] = 2, k.cb[1] = 0; break;
+    case 1: k.rb[0] = 0, k.lim[0] = 8, k.cb[0] = 80, k.rb[1] = 64, k.lim[1] = 2, k.cb[1] = 64; break;
+    case 2: k.rb[0] = 0, k.lim[0] = 8, k.cb[0] = 96; break;
+    case 3: k.rb[0] = 0, k.lim[0] = 8, k.cb[0] = 112; break;
+    case 4: k.rb[0] = 0, k.lim[0] = 8, k.cb[0] = 48; break;
+    case 5: k.rb[0] = 64, k.lim[0] = 8, k.cb[0] = 112; break;
+    case 6: k.rb[0] = 0, k.lim[0] = 4, k.cb[0] = 16, k.rb[1] = 0, k.lim[1] = 6, k.cb[1] = 32; break;
+    default: k.rb[0] = 64, k.lim[0] = 4, k.cb[0] = 80, k.rb[1] = 64, k.lim[1] = 6, k.cb[1] = 96; break;
+  }
+  return k;
+}
+
+__device__ __forceinline__ void mma_ktile_diag(const char* as, const char* bs, double (&acc)[8][4][2],
+                                               const DiagTask& tk, int g, int t) {
+#pragma unroll
+  for (int sp = 0; sp < 2; ++sp) {
+    const int kk = 4 * t + 2 * sp;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int lim = tk.lim[h];
+      if (lim == 0) continue;  // warp-uniform
+      double2 af[8], bf[2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < lim) af[i] = *reinterpret_cast<const double2*>(as + kmaj_off(tk.rb[h] + i * 8 + g, kk));
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = *reinterpret_cast<const double2*>(bs + kmaj_off(tk.cb[h] + j * 8 + g, kk));
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < lim) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][2 * h + j], af[i].x, bf[j].x);
+        }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < lim) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][2 * h + j], af[i].y, bf[j].y);
+        }
+    }
+  }
+}
+
+// epilogue of a diagonal tile (same arithmetic as `epilogue`, the strip mapping of DiagTask)
+__device__ __forceinline__ void epilogue_diag(const Params& p, const double (&acc)[8][4][2], int64_t tile, int z,
+                                              int64_t m0, int64_t n0, const DiagTask& tk, int g, int t) {
+  double* out = p.splits > 1 ? p.partial + ((int64_t)z * p.ntiles + tile) * (BM * BN) : nullptr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int h = j >> 1;
+      if (i >= tk.lim[h]) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ml = tk.rb[h] + i * 8 + g;
+        const int nl = tk.cb[h] + (j & 1) * 8 + 2 * t + e;
+        if (out) {
+          out[nl * BM + ml] = acc[i][j][e];
+          continue;
+        }
+        const int64_t m = m0 + ml, n = n0 + nl;
+        if (m >= p.M || n >= p.N || m > n) continue;
+        double v = p.alpha * acc[i][j][e];
+        if (p.beta != 0.0) v += p.beta * p.C[n * p.ldc + m];
+        if (p.row_scale) v *= p.row_scale[m];
+        if (p.col_scale) v *= p.col_scale[n];
+        if (p.col_div) v /= p.col_div[n];
+        p.C[n * p.ldc + m] = v;
+        if (m != n) p.C[m * p.ldc + n] = v;
+      }
+    }
+}
+
 template <bool AK, bool BKM, int NJ>
 __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
   const Params& p = tp.p;
@@ -412,8 +528,21 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
-  const int64_t tile = blockIdx.x;
-  const int z = blockIdx.z;
+  int64_t tile = blockIdx.x;
+  int z = blockIdx.z;
+  if (p.sym && p.splits > 1 && p.tiles_m <= GN) {
+    // small symmetric output: block order = all splits of the (full-cost) off-diagonal tiles first,
+    // then the diagonal tiles -- longest jobs first, and neighbouring CTAs still share a k range
+    const int64_t T = p.tiles_m, n_off = T * (T - 1) / 2;
+    const int64_t lin = blockIdx.x + p.ntiles * (int64_t)blockIdx.z, cut = n_off * p.splits;
+    if (lin < cut) {
+      z = (int)(lin / n_off);
+      tile = lin % n_off;
+    } else {
+      z = (int)((lin - cut) / T);
+      tile = n_off + (lin - cut) % T;
+    }
+  }
   int bi, bj;
   tile_coords(p, tile, bi, bj);
   constexpr int TBN = 32 * NJ;                 // tile width in n (4 n-warps x NJ fragments of 8)
@@ -473,6 +602,21 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (AK && BKM && NJ == 4) {
+    if (p.sym && bi == bj) {
+      const DiagTask tk = diag_task(warp);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % TSTAGES;
+        mbar_wait(&full_bar[s], (kt / TSTAGES) & 1);
+        const char* sa = sbase + s * STAGE_BYTES;
+        mma_ktile_diag(sa, sa + TILE_BYTES, acc, tk, g, t);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+      }
+      epilogue_diag(p, acc, tile, z, m0, n0, tk, g, t);
+      return;
+    }
+  }
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % TSTAGES;
     mbar_wait(&full_bar[s], (kt / TSTAGES) & 1);
@@ -535,7 +679,53 @@ int narrow_bn(int64_t N) {
   return best;
 }
 
-Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = BN) {
+// Split count of a small symmetric product whose diagonal tiles take the re-dealt path
+// (mma_ktile_diag, ~56 % of a full tile): the CTAs of a launch are handed to the SMs in block order
+// (all splits of the off-diagonal tiles, then the diagonal ones; one CTA per SM at a time), so the
+// launch ends when the slowest SM does.  Among the split counts around the default one, take the
+// one with the shortest modelled makespan (cost of a CTA in 16-deep k steps + 2 for its prologue
+// and epilogue).  A function of the shape only -- 148 is a constant here, not a device query.
+int diag_aware_splits(int T, int64_t K, int64_t base, int64_t min_k) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int64_t>, int> cache;
+  const auto key = std::make_tuple(T, K, base);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const int P = 148;
+  const int64_t n_off = (int64_t)T * (T - 1) / 2;
+  const int64_t lo = std::max<int64_t>(1, base / 2), hi = std::max<int64_t>(1, std::min<int64_t>(2 * base, K / min_k));
+  int best = (int)base;
+  double best_span = 0.0;
+  std::vector<double> heap;
+  for (int64_t s0 = lo; s0 <= hi; ++s0) {
+    const int64_t kspan = ceil_div(ceil_div(K, s0), BK) * BK;
+    const int64_t sp = std::max<int64_t>(1, ceil_div(K, kspan));
+    if (sp != s0) continue;  // not a distinct plan
+    const double n = (double)(kspan / BK);
+    const double c_full = n + 2.0, c_diag = 0.5625 * n + 2.0;
+    heap.assign(P, 0.0);  // min-heap of the SMs' free times
+    auto cmp = [](double a, double b) { return a > b; };
+    double span = 0.0;
+    for (int64_t c = 0; c < (n_off + T) * sp; ++c) {  // launch order: every full tile, then the diagonal ones
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      heap.back() += c < n_off * sp ? c_full : c_diag;
+      span = std::max(span, heap.back());
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    if (best_span == 0.0 || span < best_span * (1.0 - 1e-9)) {
+      best_span = span;
+      best = (int)sp;
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = best;
+  return best;
+}
+
+Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = BN, bool diag_aware = false) {
   Plan pl;
   pl.bn = bn;
   pl.tiles_m = (int)ceil_div(M, BM);
@@ -554,6 +744,8 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = B
     splits = std::min<int64_t>(splits, std::max<int64_t>(K / min_k, 1));
     splits = std::min<int64_t>(splits, target);  // a one-tile output over a long K (a chain merge's drift SYRK) spreads over the whole chip
     splits = std::max<int64_t>(splits, 1);
+    if (diag_aware && sym && bn == BN && splits > 1 && pl.tiles_m >= 2 && pl.tiles_m <= GN)
+      splits = diag_aware_splits(pl.tiles_m, K, splits, min_k);
   }
   pl.kspan = ceil_div(ceil_div(K, splits), BK) * BK;
   splits = std::max<int64_t>(1, ceil_div(K, std::max<int64_t>(pl.kspan, 1)));
@@ -689,7 +881,9 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   const bool tma_ok = aligned16 && !A.table && !B.table && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31);
   // narrow n tiles (96 / 64 wide) exist on the TMA path with a K-major B operand only
   const int bn = (tma_ok && b_kmajor && !sym && !b_upper && !tl_nosplit) ? narrow_bn(N) : BN;
-  apply_plan(make_plan(M, N, K, sym, b_upper, bn));
+  // diagonal tiles of a symmetric K-major x K-major product take the re-dealt path on the TMA kernel
+  const bool diag_aware = tma_ok && a_kmajor && b_kmajor && sym && !b_upper && !tl_nosplit;
+  apply_plan(make_plan(M, N, K, sym, b_upper, bn, diag_aware));
   if (tl_nosplit) {
     p.splits = 1;
     p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
@@ -731,6 +925,7 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
   if (M <= 0 || N <= 0) return 0;
   size_t need = gemm::make_plan(M, N, K, sym, b_upper).ws_bytes;
+  if (sym && !b_upper) need = std::max(need, gemm::make_plan(M, N, K, sym, b_upper, gemm::BN, true).ws_bytes);
   if (!sym && !b_upper)  // the narrow-tile plan of the same shape (gemm_run picks it on the TMA path)
     need = std::max(need, gemm::make_plan(M, N, K, sym, b_upper, gemm::narrow_bn(N)).ws_bytes);
   return need;
