@@ -79,47 +79,40 @@ struct Layout {
 constexpr int GN = 8;
 
 __device__ __forceinline__ void tile_coords(const Params& p, int64_t t, int& bi, int& bj) {
-  if (p.sym && p.tiles_m <= GN) {
-    // one super-column: the off-diagonal tiles row by row, then the diagonal tiles (which cost about
-    // half a tile on the TMA path, mma_ktile_diag) -- the order make_plan's makespan model assumes
+  if (p.sym) {
+    // strictly upper triangle (bi < bj) in super-columns of GN tile columns -- group g holds columns
+    // [g GN, g GN + gn): first the full rows bi < g GN (gn tiles each), then the group's own triangle
+    // -- and the T diagonal tiles last.  A diagonal tile costs about half a tile on the TMA path
+    // (mma_ktile_diag): in the middle of a launch it would take its SM out of step with the wave
+    // that shares its operand panels in L2 (ncu: root Gram DRAM reads 115 -> 177 GB); at the end
+    // the diagonal tiles fill the last, partial wave.  Also the order make_plan's makespan model
+    // and the kernel's longest-first block order of small split-K outputs assume.
     const int T = p.tiles_m;
     const int64_t off = (int64_t)T * (T - 1) / 2;
     if (t >= off) {
       bi = bj = (int)(t - off);
     } else {
-      int64_t r = t;
-      int i = 0;
-      while (r >= T - 1 - i) {
-        r -= T - 1 - i;
-        ++i;
+      int g = 0;
+      while (true) {
+        const int64_t c1 = (int64_t)min(T, (g + 1) * GN);
+        if (c1 * (c1 - 1) / 2 > t) break;
+        ++g;
       }
-      bi = i;
-      bj = i + 1 + (int)r;
-    }
-  } else if (p.sym) {
-    // upper triangle (bi <= bj) in super-columns of GN tile columns: group g holds columns
-    // [g GN, g GN + gn), first the full rows bi < g GN (gn tiles each), then the triangle
-    const int T = p.tiles_m;
-    int g = 0;
-    while (true) {
-      const int64_t c1 = (int64_t)min(T, (g + 1) * GN);
-      if (c1 * (c1 + 1) / 2 > t) break;
-      ++g;
-    }
-    const int c0 = g * GN, gn = min(T, c0 + GN) - c0;
-    int64_t r = t - (int64_t)c0 * (c0 + 1) / 2;
-    if (r < (int64_t)c0 * gn) {
-      bi = (int)(r / gn);
-      bj = c0 + (int)(r % gn);
-    } else {
-      r -= (int64_t)c0 * gn;
-      int i = 0;
-      while (r >= gn - i) {
-        r -= gn - i;
-        ++i;
+      const int c0 = g * GN, gn = min(T, c0 + GN) - c0;
+      int64_t r = t - (int64_t)c0 * (c0 - 1) / 2;
+      if (r < (int64_t)c0 * gn) {
+        bi = (int)(r / gn);
+        bj = c0 + (int)(r % gn);
+      } else {
+        r -= (int64_t)c0 * gn;
+        int i = 0;
+        while (r >= gn - 1 - i) {
+          r -= gn - 1 - i;
+          ++i;
+        }
+        bi = c0 + i;
+        bj = c0 + i + 1 + (int)r;
       }
-      bi = c0 + i;
-      bj = c0 + i + (int)r;
     }
   } else {
     const int64_t per_group = (int64_t)p.tiles_m * GN;

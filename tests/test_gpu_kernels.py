@@ -40,6 +40,46 @@ def test_gram_matches_numpy(d, m):
     assert np.max(np.abs(g - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(d)
 
 
+@pytest.mark.parametrize("d,m", [(20000, 256), (30000, 384), (50000, 640), (9000, 1000), (40000, 130),
+                                 (200000, 512)])
+def test_gram_small_symmetric_outputs_split(d, m):
+    """Small symmetric outputs (2..8 tile columns, split-K): the re-dealt diagonal tiles, the
+    longest-first block order and the makespan-modelled split count (hp_gemm.cu, diag_aware_splits)
+    against float64 NumPy (gramian, pod.py:208-211)."""
+    g0 = torch.Generator(device="cuda").manual_seed(d + m)
+    A = D.DevMat.empty(d, m)
+    A.tensor().copy_(torch.randn(d, m, generator=g0, device="cuda", dtype=torch.float64))
+    G = D.DevMat.empty(m, m)
+    w = ws(lib.hp_gram_workspace_bytes(d, m))
+    N.check(lib.hp_gram(A.vecset(), d, m, None, G.ptr, G.ld, w.data_ptr(), w.numel(), st()), "gram")
+    g = G.to_numpy()
+    a = A.to_numpy()
+    ref = a.T @ a
+    assert np.array_equal(g, g.T)
+    assert np.max(np.abs(g - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(d)
+
+
+@pytest.mark.parametrize("n", [128, 200, 512, 640])
+def test_diagonal_tile_path_is_bitwise_the_regular_path(n):
+    """A diagonal block of a Gramian through the symmetric launch (diagonal tiles re-dealt over the
+    consumer warps, mma_ktile_diag) against the same block as a plain pair product (regular 2 x 4
+    warp grid): both unsplit, so every entry with row <= column must agree bit for bit."""
+    d = 3000
+    rng = np.random.default_rng(n)
+    U = D.upload(np.asfortranarray(rng.standard_normal((d, n))))
+    sig = torch.tensor(10.0 ** rng.uniform(-2, 0, n), device="cuda")
+    sym = D.DevMat.empty(n, n, zero=True)
+    full = D.DevMat.empty(n, n, zero=True)
+    N.check(lib.hp_gram_pair(U.vecset(), sig.data_ptr(), n, U.vecset(), sig.data_ptr(), n, d, 1, sym.ptr, sym.ld,
+                             st()), "symmetric pair")
+    N.check(lib.hp_gram_pair(U.vecset(), sig.data_ptr(), n, U.vecset(), sig.data_ptr(), n, d, 0, full.ptr, full.ld,
+                             st()), "plain pair")
+    a, b = sym.to_numpy(), full.to_numpy()
+    iu = np.triu_indices(n)
+    assert np.array_equal(a[iu], b[iu])
+    assert np.array_equal(a, a.T)
+
+
 @pytest.mark.parametrize("odd", [False, True])
 def test_gram_colscale_and_table(odd):
     rng = np.random.default_rng(5)

@@ -53,6 +53,34 @@ def launches():
     print("\n".join(out[:25]))
 
 
+def traffic(h, u, v, source):
+    """profiles/traffic.json (read by bench.py's roofline.traffic): DRAM bytes of the config-1 root
+    Gram SYRK launch from its ncu --set full capture."""
+    import json
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+    def val(k):
+        i = h.index(k)
+        return float(v[i].replace(",", "")) * scale.get(u[i], 1.0)
+
+    rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+    i = h.index("gpu__time_duration.sum")
+    ms = float(v[i].replace(",", "")) * {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}.get(u[i].replace("econd", ""), 1.0)
+    entry = {"kernel": "gemm_tma_kernel<1, 1, 4> (root Gram SYRK, m = 8192, d = 200000)",
+             "dram_bytes": int(rd + wr), "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
+             "algorithmic_bytes": 13650000000, "duration_ms": ms,
+             "source": f"{source} (ncu --set full --clock-control none: dram__bytes_read.sum + "
+                       f"dram__bytes_write.sum of one launch)"}
+    path = os.path.join(dst, "traffic.json")
+    try:
+        data = json.load(open(path))
+    except (OSError, ValueError):
+        data = {}
+    data["gram_syrk_m8192_d200000"] = entry
+    json.dump(data, open(path, "w"), indent=1)
+    print("traffic.json:", entry)
+
+
 def reports():
     for rep in sorted(glob.glob(os.path.join(src, f"{tag}_*.ncu-rep"))):
         name = os.path.basename(rep)[len(tag) + 1: -len(".ncu-rep")]
@@ -79,6 +107,8 @@ def reports():
             out.append("")
         open(os.path.join(dst, f"{tag}_{name}_metrics.txt"), "w").write("\n".join(out) + "\n")
         print("\n".join(out))
+        if name == "gemm_gram8192":
+            traffic(h, u, rows[2], f"profiles/{tag}_{name}_metrics.txt")
 
 
 launches()
