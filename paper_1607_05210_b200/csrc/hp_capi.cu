@@ -38,6 +38,7 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
              const double* col_div, int sym, int b_upper, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper);
 void gemm_set_nosplit(bool on);
+void gemm_set_wavesplit(bool on);
 bool gemm_plan_is_single_split(int64_t M, int64_t N, int64_t K, int sym);
 size_t syev_workspace_bytes(int64_t n);
 int64_t syev_padded_order(int64_t n);
@@ -133,8 +134,11 @@ static constexpr double kSinglePassDrift = 1e-1;
 static int gram_sym(const double* X, int64_t ldx, int64_t d, int64_t N, double* C, int64_t ldc, void* ws,
                     size_t wsb, cudaStream_t st) {
   VecSet a{X, ldx, nullptr};
-  return gemm_run(true, true, N, N, d, a, a, (ldx % 2 == 0), 1.0, 0.0, C, ldc, nullptr, nullptr, nullptr, 1, 0, ws,
-                  wsb, st);
+  gemm_set_wavesplit(true);  // X^T X only feeds the drift and the Cholesky of CholQR
+  const int rc = gemm_run(true, true, N, N, d, a, a, (ldx % 2 == 0), 1.0, 0.0, C, ldc, nullptr, nullptr, nullptr, 1,
+                          0, ws, wsb, st);
+  gemm_set_wavesplit(false);
+  return rc;
 }
 
 __global__ void add_diag(double* C, int64_t ldc, int64_t n, double s) {

@@ -523,8 +523,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) gemm_tma_kernel(const __grid_cons
 
   int64_t tile = blockIdx.x;
   int z = blockIdx.z;
-  if (p.sym && p.splits > 1 && p.tiles_m <= GN) {
-    // small symmetric output: block order = all splits of the (full-cost) off-diagonal tiles first,
+  if (p.sym && p.splits > 1) {
+    // split symmetric output: block order = all splits of the (full-cost) off-diagonal tiles first,
     // then the diagonal tiles -- longest jobs first, and neighbouring CTAs still share a k range
     const int64_t T = p.tiles_m, n_off = T * (T - 1) / 2;
     const int64_t lin = blockIdx.x + p.ntiles * (int64_t)blockIdx.z, cut = n_off * p.splits;
@@ -718,7 +718,55 @@ int diag_aware_splits(int T, int64_t K, int64_t base, int64_t min_k) {
   return best;
 }
 
-Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = BN, bool diag_aware = false) {
+// Split count (1..4) of a LARGE symmetric product whose tile count leaves the last wave mostly empty
+// (666 tiles on 148 SMs = 4.5 waves cost 5): the same makespan model as diag_aware_splits over the
+// kernel's block order (all splits of the off-diagonal tiles, then the diagonal ones), plus the
+// second-pass reduction of the partial tiles.  Only used where the caller allows it
+// (gemm_set_wavesplit: the orthonormality SYRKs); a split is taken only for a gain above 3 %.
+int wave_splits(int T, int64_t K) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, int> cache;
+  const auto key = std::make_pair(T, K);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const int P = 148;
+  const int64_t n_off = (int64_t)T * (T - 1) / 2;
+  int best = 1;
+  double best_span = 0.0, span1 = 0.0;
+  std::vector<double> heap;
+  for (int64_t s0 = 1; s0 <= 4 && K / s0 >= 512; ++s0) {
+    const int64_t kspan = ceil_div(ceil_div(K, s0), BK) * BK;
+    const int64_t sp = std::max<int64_t>(1, ceil_div(K, kspan));
+    if (sp != s0) continue;
+    const double n = (double)(kspan / BK);
+    const double c_full = n + 2.0, c_diag = 0.5625 * n + 2.0;
+    heap.assign(P, 0.0);
+    auto cmp = [](double a, double b) { return a > b; };
+    double span = 0.0;
+    for (int64_t c = 0; c < (n_off + T) * sp; ++c) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      heap.back() += c < n_off * sp ? c_full : c_diag;
+      span = std::max(span, heap.back());
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    if (sp > 1) span += 0.025 * (double)sp * (double)(n_off + T);  // partial tiles written and re-read
+    if (sp == 1) span1 = span;
+    if (best_span == 0.0 || span < best_span) {
+      best_span = span;
+      best = (int)sp;
+    }
+  }
+  if (best > 1 && !(best_span < 0.97 * span1)) best = 1;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = best;
+  return best;
+}
+
+Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = BN, bool diag_aware = false,
+               bool wave_split = false) {
   Plan pl;
   pl.bn = bn;
   pl.tiles_m = (int)ceil_div(M, BM);
@@ -739,6 +787,8 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int sym, int b_upper, int bn = B
     splits = std::max<int64_t>(splits, 1);
     if (diag_aware && sym && bn == BN && splits > 1 && pl.tiles_m >= 2 && pl.tiles_m <= GN)
       splits = diag_aware_splits(pl.tiles_m, K, splits, min_k);
+  } else if (wave_split && diag_aware && sym && !b_upper && bn == BN) {
+    splits = wave_splits(pl.tiles_m, K);
   }
   pl.kspan = ceil_div(ceil_div(K, splits), BK) * BK;
   splits = std::max<int64_t>(1, ceil_div(K, std::max<int64_t>(pl.kspan, 1)));
@@ -826,6 +876,11 @@ int launch_tma(const Params& p, cudaStream_t st, bool& done) {
 // corresponding block of the monolithic launch bit for bit (hp_gram_pair).
 static thread_local bool tl_nosplit = false;
 void gemm_set_nosplit(bool on) { tl_nosplit = on; }
+// Calling-thread switch: the next symmetric gemm_run calls may split a LARGE output's contraction to
+// even out the last wave (gemm::wave_splits).  Off for the node Gramians, whose pair blocks must equal
+// the monolithic launch bit for bit; on for the orthonormality SYRKs (drift, CholQR).
+static thread_local bool tl_wavesplit = false;
+void gemm_set_wavesplit(bool on) { tl_wavesplit = on; }
 bool gemm_plan_is_single_split(int64_t M, int64_t N, int64_t K, int sym) {
   return gemm::make_plan(M, N, K, sym, 0).splits == 1;
 }
@@ -876,7 +931,7 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
   const int bn = (tma_ok && b_kmajor && !sym && !b_upper && !tl_nosplit) ? narrow_bn(N) : BN;
   // diagonal tiles of a symmetric K-major x K-major product take the re-dealt path on the TMA kernel
   const bool diag_aware = tma_ok && a_kmajor && b_kmajor && sym && !b_upper && !tl_nosplit;
-  apply_plan(make_plan(M, N, K, sym, b_upper, bn, diag_aware));
+  apply_plan(make_plan(M, N, K, sym, b_upper, bn, diag_aware, tl_wavesplit));
   if (tl_nosplit) {
     p.splits = 1;
     p.kspan = ceil_div(std::max<int64_t>(K, 1), BK) * BK;
@@ -918,7 +973,9 @@ int gemm_run(bool a_kmajor, bool b_kmajor, int64_t M, int64_t N, int64_t K, VecS
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int sym, int b_upper) {
   if (M <= 0 || N <= 0) return 0;
   size_t need = gemm::make_plan(M, N, K, sym, b_upper).ws_bytes;
-  if (sym && !b_upper) need = std::max(need, gemm::make_plan(M, N, K, sym, b_upper, gemm::BN, true).ws_bytes);
+  if (sym && !b_upper)
+    need = std::max({need, gemm::make_plan(M, N, K, sym, b_upper, gemm::BN, true).ws_bytes,
+                     gemm::make_plan(M, N, K, sym, b_upper, gemm::BN, true, true).ws_bytes});
   if (!sym && !b_upper)  // the narrow-tile plan of the same shape (gemm_run picks it on the TMA path)
     need = std::max(need, gemm::make_plan(M, N, K, sym, b_upper, gemm::narrow_bn(N)).ws_bytes);
   return need;
