@@ -248,6 +248,45 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
         }
     return;
   }
+  if constexpr (!AK) {
+    // M-major A: a thread's 8 row fragments are 8 CONSECUTIVE rows of one output column -- stored as
+    // four 16-byte words instead of eight scattered 8-byte ones (same arithmetic, same order)
+    if (p.beta == 0.0 && !p.sym && (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) {
+      const int64_t mb = m0 + wm * 64 + g * 8;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t n = n0 + wn * (8 * NJ) + (BKM ? j * 8 + 2 * t + e : (2 * t + e) * 4 + j);
+          if (n >= p.N) continue;
+          const bool cs = p.col_scale != nullptr, cd = p.col_div != nullptr;
+          const double csv = cs ? p.col_scale[n] : 1.0, cdv = cd ? p.col_div[n] : 1.0;
+          double* dst = p.C + n * p.ldc + mb;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            if (mb + i >= p.M) break;
+            double v0 = p.alpha * acc[i][j][e], v1 = p.alpha * acc[i + 1][j][e];
+            if (p.row_scale) {
+              v0 *= p.row_scale[mb + i];
+              if (mb + i + 1 < p.M) v1 *= p.row_scale[mb + i + 1];
+            }
+            if (cs) {
+              v0 *= csv;
+              v1 *= csv;
+            }
+            if (cd) {
+              v0 /= cdv;
+              v1 /= cdv;
+            }
+            if (mb + i + 1 < p.M)
+              *reinterpret_cast<double2*>(dst + i) = make_double2(v0, v1);
+            else
+              dst[i] = v0;
+          }
+        }
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
