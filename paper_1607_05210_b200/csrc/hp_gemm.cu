@@ -50,7 +50,7 @@ struct Params {
   const double* row_scale;
   const double* col_scale;
   const double* col_div;
-  int sym;
+  int sym;  // 0 general; 1 symmetric output: tiles bi <= bj computed, entries mirrored; 2 the same, upper part only (no mirror)
   int b_upper;
   int splits;
   int64_t kspan;
@@ -251,7 +251,10 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
   if constexpr (!AK) {
     // M-major A: a thread's 8 row fragments are 8 CONSECUTIVE rows of one output column -- stored as
     // four 16-byte words instead of eight scattered 8-byte ones (same arithmetic, same order)
-    if (p.beta == 0.0 && !p.sym && (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) {
+    // (also the read-modify-write of a symmetric update on a tile strictly above the diagonal, where
+    // every entry is wanted; sym == 1 adds the mirrored entries as single words)
+    const bool whole = !p.sym || m0 + BM <= n0;
+    if (whole && (p.beta == 0.0 || p.sym) && (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) {
       const int64_t mb = m0 + wm * 64 + g * 8;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
@@ -266,6 +269,15 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
           for (int i = 0; i < 8; i += 2) {
             if (mb + i >= p.M) break;
             double v0 = p.alpha * acc[i][j][e], v1 = p.alpha * acc[i + 1][j][e];
+            if (p.beta != 0.0) {
+              if (mb + i + 1 < p.M) {
+                const double2 old = *reinterpret_cast<const double2*>(dst + i);
+                v0 += p.beta * old.x;
+                v1 += p.beta * old.y;
+              } else {
+                v0 += p.beta * dst[i];
+              }
+            }
             if (p.row_scale) {
               v0 *= p.row_scale[mb + i];
               if (mb + i + 1 < p.M) v1 *= p.row_scale[mb + i + 1];
@@ -282,6 +294,10 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
               *reinterpret_cast<double2*>(dst + i) = make_double2(v0, v1);
             else
               dst[i] = v0;
+            if (p.sym == 1) {
+              p.C[(mb + i) * p.ldc + n] = v0;
+              if (mb + i + 1 < p.M) p.C[(mb + i + 1) * p.ldc + n] = v1;
+            }
           }
         }
       return;
@@ -303,7 +319,7 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
         if (p.col_scale) v *= p.col_scale[n];
         if (p.col_div) v /= p.col_div[n];
         p.C[n * p.ldc + m] = v;
-        if (p.sym && m != n) p.C[m * p.ldc + n] = v;
+        if (p.sym == 1 && m != n) p.C[m * p.ldc + n] = v;
       }
 }
 
@@ -545,7 +561,7 @@ __device__ __forceinline__ void epilogue_diag(const Params& p, const double (&ac
         if (p.col_scale) v *= p.col_scale[n];
         if (p.col_div) v /= p.col_div[n];
         p.C[n * p.ldc + m] = v;
-        if (m != n) p.C[m * p.ldc + n] = v;
+        if (p.sym == 1 && m != n) p.C[m * p.ldc + n] = v;
       }
     }
 }
@@ -681,7 +697,7 @@ __global__ void splitk_reduce(Params p) {
   if (p.col_scale) v *= p.col_scale[n];
   if (p.col_div) v /= p.col_div[n];
   p.C[n * p.ldc + m] = v;
-  if (p.sym && m != n) p.C[m * p.ldc + n] = v;
+  if (p.sym == 1 && m != n) p.C[m * p.ldc + n] = v;
 }
 
 struct Plan {

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(PT) pstrf_panel(Params p) {
       } else if (p.d[i] == -INFINITY) {
         li = 0.0;  // already pivoted: L is lower triangular in pivot order
       } else {
-        double s = acol[i];
+        double s = i <= pv ? acol[i] : p.A[i * p.lda + pv];  // only the upper part of A is kept up to date
         for (int t = p.k0; t < j; ++t) s -= p.L[(int64_t)t * p.ldl + i] * s_lp[t - p.k0];
         li = s * rl;
         p.d[i] -= li * li;
@@ -274,7 +274,12 @@ __global__ void __launch_bounds__(PT) pstrf_panel_sm(Params p) {
     const double* acol = p.A + (int64_t)pv * p.lda;
     const int row_first = tid / RT;
     double a_first = 0.0;
-    if (sub == 0 && row_first < nr) a_first = acol[r0 + row_first];
+    // (only the upper part of the working matrix is kept up to date by the trailing updates:
+    // entry (i, pv) is read as (min, max))
+    if (sub == 0 && row_first < nr) {
+      const int64_t i0 = r0 + row_first;
+      a_first = i0 <= pv ? acol[i0] : p.A[i0 * p.lda + pv];
+    }
     __syncthreads();
     const double rl = 1.0 / ljj;
     for (int rb = 0; rb < nr; rb += PT / RT) {
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(PT) pstrf_panel_sm(Params p) {
         } else if (di == -INFINITY) {
           li = 0.0;  // already pivoted: L is lower triangular in pivot order
         } else {
-          const double a = rb == 0 ? a_first : acol[i];
+          const double a = rb == 0 ? a_first : (i <= pv ? acol[i] : p.A[i * p.lda + pv]);
           li = (a + part) * rl;
           s_d[il] = di - li * li;
         }
@@ -511,8 +516,10 @@ int pstrf_run(const double* G, int64_t ldg, int64_t m, double* L, int64_t ldl, i
     if (done < p.k1 || done >= m) break;
     // trailing update of the whole working matrix: A -= L_panel L_panel^T
     VecSet a{L + k0 * ldl, ldl, nullptr};
+    // (upper part only, sym = 2: the panel kernels read entry (i, pv) as (min, max), and the mirror
+    // was a third of this update's memory traffic, all of it scattered 8-byte stores)
     int rc = gemm_run(false, false, m, m, p.k1 - k0, a, a, (ldl % 2 == 0), -1.0, 1.0, A, lda, nullptr, nullptr,
-                      nullptr, 1, 0, gws, gwsb, st);
+                      nullptr, 2, 0, gws, gwsb, st);
     if (rc) return rc;
   }
   *rank_out = host_rank;
