@@ -61,7 +61,8 @@ int hp_device_sm_count(int device);
  * C(m,n) *= row_scale[m] * col_scale[n], C(m,n) /= col_div[n] (each nullable).
  *   a_kmajor: A(m,k) = A.vec(m)[k]  else A(m,k) = A.vec(k)[m]
  *   b_kmajor: B(k,n) = B.vec(n)[k]  else B(k,n) = B.vec(k)[n]
- *   sym:      M == N, only the upper triangle is computed and mirrored
+ *   sym:      1: M == N, only the upper triangle is computed and mirrored;
+ *             2: the same without the mirror (the lower triangle of C is left untouched)
  *   b_upper:  B is upper triangular (B(k,n) = 0 for k > n)
  * Long contractions are split over K with a fixed-order reduction
  * (deterministic; the plan depends only on M, N, K). */

@@ -254,8 +254,63 @@ __device__ __forceinline__ void epilogue(const Params& p, const double (&acc)[8]
     // (also the read-modify-write of a symmetric update on a tile strictly above the diagonal, where
     // every entry is wanted; sym == 1 adds the mirrored entries as single words)
     const bool whole = !p.sym || m0 + BM <= n0;
-    if (whole && (p.beta == 0.0 || p.sym) && (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) {
+    if (whole && (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) {
       const int64_t mb = m0 + wm * 64 + g * 8;
+      if constexpr (!BKM && NJ == 4) {
+        // symmetric update with a mirror and an N-major B (the tridiagonalisation's rank-2k updates): a
+        // thread's fragments j, j + 1 are CONSECUTIVE columns, so the mirrored entries of one row go
+        // out as 16-byte words too
+        if (p.sym == 1 && !p.row_scale && !p.col_scale && !p.col_div) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int jp = 0; jp < 4; jp += 2) {
+              const int64_t na = n0 + wn * 32 + (2 * t + e) * 4 + jp;
+              if (na >= p.N) continue;
+              const bool hb = na + 1 < p.N;
+              double* da = p.C + na * p.ldc + mb;
+              double* db = da + p.ldc;
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                if (mb + i >= p.M) break;
+                const bool h1 = mb + i + 1 < p.M;
+                double a0 = p.alpha * acc[i][jp][e], a1 = p.alpha * acc[i + 1][jp][e];
+                double b0 = p.alpha * acc[i][jp + 1][e], b1 = p.alpha * acc[i + 1][jp + 1][e];
+                if (p.beta != 0.0) {
+                  if (h1) {
+                    const double2 oa = *reinterpret_cast<const double2*>(da + i);
+                    a0 += p.beta * oa.x;
+                    a1 += p.beta * oa.y;
+                    if (hb) {
+                      const double2 ob = *reinterpret_cast<const double2*>(db + i);
+                      b0 += p.beta * ob.x;
+                      b1 += p.beta * ob.y;
+                    }
+                  } else {
+                    a0 += p.beta * da[i];
+                    if (hb) b0 += p.beta * db[i];
+                  }
+                }
+                if (h1) {
+                  *reinterpret_cast<double2*>(da + i) = make_double2(a0, a1);
+                  if (hb) *reinterpret_cast<double2*>(db + i) = make_double2(b0, b1);
+                } else {
+                  da[i] = a0;
+                  if (hb) db[i] = b0;
+                }
+                double* r0 = p.C + (mb + i) * p.ldc + na;  // mirrored: row mb + i, columns na, na + 1
+                if (hb) {
+                  *reinterpret_cast<double2*>(r0) = make_double2(a0, b0);
+                  if (h1) *reinterpret_cast<double2*>(r0 + p.ldc) = make_double2(a1, b1);
+                } else {
+                  r0[0] = a0;
+                  if (h1) r0[p.ldc] = a1;
+                }
+              }
+            }
+          return;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
 #pragma unroll

@@ -130,6 +130,49 @@ def test_gemm_nt_sym_and_upper():
     assert np.allclose(Y.to_numpy(), x @ l.T, rtol=1e-12, atol=1e-11)
 
 
+@pytest.mark.parametrize("bk", [0, 1])
+@pytest.mark.parametrize("M,K", [(200, 64), (515, 128), (1000, 130)])
+def test_gemm_symmetric_update_modes(M, K, bk):
+    """C -= P P^T with an M-major A (the pivoted Cholesky's and the tridiagonalisation's trailing
+    updates): sym = 1 writes both triangles (16-byte words and, with an N-major B, 16-byte mirrored
+    words on the tiles above the diagonal); sym = 2 updates the upper triangle only and must leave
+    the strictly lower part of C untouched.  Ragged last tiles in both directions."""
+    rng = np.random.default_rng(M + K + bk)
+    p = rng.standard_normal((M, K))
+    c0 = rng.standard_normal((M, M))
+    c0 = c0 + c0.T
+    P = D.upload(p)
+    Bop = P if bk == 0 else D.upload(np.asfortranarray(p.T))  # K-major B: vector n holds p[n, :]
+    want = c0 - p @ p.T
+    for sym in (1, 2):
+        C = D.upload(c0)
+        w = ws(lib.hp_gemm_workspace_bytes(M, M, K, sym, 0))
+        N.check(lib.hp_gemm(0, bk, M, M, K, P.vecset(), Bop.vecset(), -1.0, 1.0, C.ptr, C.ld, None, None, None, sym,
+                            0, w.data_ptr(), w.numel(), st()), "symmetric update")
+        got = C.to_numpy()
+        iu = np.triu_indices(M)
+        assert np.allclose(got[iu], want[iu], rtol=1e-12, atol=1e-11)
+        il = np.tril_indices(M, -1)
+        if sym == 1:
+            assert np.array_equal(got, got.T)
+        else:
+            assert np.array_equal(got[il], c0[il])
+
+
+@pytest.mark.parametrize("M,N_,K", [(300, 70, 33), (2000, 257, 512)])
+def test_gemm_accumulate_beta(M, N_, K):
+    """C = 0.5 C - A B with an M-major A: the read-modify-write epilogue (16-byte words)."""
+    rng = np.random.default_rng(M * 3 + N_ + K)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N_))
+    c0 = rng.standard_normal((M, N_))
+    A, B, C = D.upload(a), D.upload(b), D.upload(c0)
+    w = ws(lib.hp_gemm_workspace_bytes(M, N_, K, 0, 0))
+    N.check(lib.hp_gemm(0, 1, M, N_, K, A.vecset(), B.vecset(), -1.0, 0.5, C.ptr, C.ld, None, None, None, 0, 0,
+                        w.data_ptr(), w.numel(), st()), "gemm")
+    assert np.allclose(C.to_numpy(), 0.5 * c0 - a @ b, rtol=1e-12, atol=1e-11)
+
+
 @pytest.mark.parametrize("ak,bk", [(1, 1), (0, 1), (0, 0), (1, 0)])
 @pytest.mark.parametrize("M,N_,K", [(1, 1, 1), (130, 257, 37), (256, 128, 40_001), (517, 300, 16), (64, 700, 4098)])
 def test_gemm_layouts_edges(ak, bk, M, N_, K):
